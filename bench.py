@@ -1,0 +1,471 @@
+#!/usr/bin/env python
+"""Rendered env-steps/sec on B200 (BASELINE.json metric), one JSON line.
+
+Workload (BASELINE.json north_star target / configs[3]): Humanoid stand-in
+(humanoid_lite, 13 links, 1248 triangles) with video distractors, 4096 envs
+per GPU, 84x84 RGB, the reference's synthetic video pack resident in HBM.
+
+A "step" = one rendered env-step for every env: given the pose batch of
+step t (resident in HBM), the fused kernel advances the distractors
+(ping-pong cursors), rasterizes, composites the video background and writes
+the uint8 observation to HBM -- ONE kernel launch (pxr_render_step).
+
+  value  device-timed (CUDA events on the launching stream, max over ranks)
+         env-steps/s of the whole job, inputs already in HBM;
+  e2e    the same through the C ABI with HOST buffers: pinned-host poses
+         H2D + fused step + obs D2H to pinned host, every step, 2 streams;
+  --impl reference   the reference's CPU path (the oracle port of
+         render_robot_batch + advance_distractors + apply_video, oracle/)
+         on all host cores, same workload, same metric.
+
+Multi-GPU: torchrun, one process per GPU; rank r renders envs
+[r*B, (r+1)*B) (env_offset = r*B, logical_batch = world*B) -- no collective
+on the hot path; NCCL only for the max-time reduce and a final stats gather.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "rendered env-steps/sec vs #envs at 1/2/4/8 B200; % HBM roofline"
+UNIT = "env-steps/s"
+DEFAULT_MODEL = "Humanoid"
+DEFAULT_ENVS = 4096
+DEFAULT_MODE = "video"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default=DEFAULT_MODEL)
+    ap.add_argument("--envs", type=int, default=DEFAULT_ENVS, help="envs per GPU")
+    ap.add_argument("--mode", default=DEFAULT_MODE, choices=["none", "color", "video"])
+    ap.add_argument("--grayscale", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def read_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload_tag):
+    """Per-launch DRAM bytes of the fused kernel from the committed ncu
+    capture summary (profiles/ncu_summary.json), if it matches."""
+    path = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get("workloads", {}).get(workload_tag)
+        if e:
+            return float(e["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled while the GPU is busy."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- ours
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2502_00021_b200 import _native
+    from paper_2502_00021_b200.bench_support import Workload
+
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    B = args.envs
+    w = Workload(args.model, B, args.mode, seed=0, env_offset=rank * B,
+                 logical_batch=world * B, grayscale=args.grayscale, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    n_pose_sets = 8
+    obs_bytes = B * w.obs_bytes_per_env()
+    l2 = 126 * 2**20
+    n_out = max(2, -(-3 * l2 // obs_bytes))  # obs ring footprint > 3x L2
+    with torch.cuda.stream(stream):
+        pose_sets = [w.poses(t, out=torch.empty_like(w.poses_buf), stream=stream).clone()
+                     for t in range(n_pose_sets)]
+        outs = [torch.empty_like(w.obs) for _ in range(n_out)]
+    torch.cuda.synchronize(dev)
+
+    def one(t):
+        w.render(pose_sets[t % n_pose_sets], t, out_obs=outs[t % n_out], stream=stream)
+
+    # warm-up (untimed), then a short soak so clocks settle
+    for t in range(max(3, args.warmup)):
+        one(t)
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local)
+    sampler.start()
+    soak_end = time.time() + 1.0
+    t_ = 0
+    while time.time() < soak_end:
+        for _ in range(20):
+            one(t_)
+            t_ += 1
+        torch.cuda.synchronize(dev)
+
+    # ---- timed region: K fused launches ----------------------------------
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for k in range(args.steps):
+        one(args.warmup + k)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        tdist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    # keep the GPU busy briefly after the window so the sampler brackets it
+    for k in range(20):
+        one(k)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+
+    # per-launch duration of the dominant (only) kernel inside the region
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(ms_t, op=tdist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    total_steps = world * B * args.steps
+    value = total_steps / (ms_max / 1e3)
+    per_launch_s = (ms / 1e3) / args.steps
+
+    # ---- e2e through the C ABI with host buffers --------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, w, dev, world, rank)
+
+    # ---- final stats gather (NCCL) -----------------------------------------
+    stats = torch.tensor([B * args.steps, ms, rank], dtype=torch.float64, device=dev)
+    if world > 1:
+        allst = [torch.empty_like(stats) for _ in range(world)]
+        tdist.all_gather(allst, stats)
+        tdist.destroy_process_group()
+
+    if rank != 0:
+        return None
+    peak, peak_src = read_peaks()
+    bytes_per_env = w.obs_bytes_per_env() + 24 * w.n_links + w.state_bytes_per_env()
+    achieved = bytes_per_env * B / per_launch_s / 1e9
+    tag = f"{args.model}-{args.mode}-{B}{'-gray' if args.grayscale else ''}"
+    traffic = ncu_traffic(tag)
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64/f32 raster, u8 RGB out",
+        "data": "synthetic: on-device pose source (reference reset keys + joint oscillation, "
+                "f64 FK); reference synthetic video pack (seed 2024, 4x60x64x64) in HBM",
+        "config": {
+            "workload": f"{args.model} ({w.spec.name}, {w.n_links} links, "
+                        f"{w.geom.triangle_count} tris), {B} envs/GPU, {args.mode} distractors, "
+                        f"{w.width}x{w.height} {'gray' if args.grayscale else 'RGB'}",
+            "model": w.spec.name, "envs_per_gpu": B, "global_envs": world * B,
+            "mode": args.mode, "resolution": [w.height, w.width],
+            "parallelism": f"env-sharded x{world} (no hot-path collective)",
+            "l2": f"obs ring of {n_out} buffers ({n_out * obs_bytes / 2**20:.0f} MiB > L2) "
+                  f"+ {n_pose_sets} resident pose sets",
+        },
+        "roofline": {
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": traffic,
+            "bytes_per_env_step": bytes_per_env,
+            "peak_source": peak_src,
+            "kernel": "render_step_kernel",
+        },
+        "gpu_launches": args.steps,
+        "e2e": e2e,
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(args, w, seconds=args.cpu_seconds)
+    return line
+
+
+def run_e2e(args, w, dev, world, rank):
+    """Host poses (pinned) -> H2D -> fused step -> D2H obs (pinned), every
+    step, double-buffered over two streams; device-timed with events."""
+    import torch
+    import torch.distributed as tdist
+
+    B = w.batch
+    host_poses = [w.poses(t).cpu().pin_memory() for t in range(2)]
+    host_obs = [torch.empty(w.obs.shape, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    dev_poses = [torch.empty_like(w.poses_buf) for _ in range(2)]
+    dev_obs = [torch.empty_like(w.obs) for _ in range(2)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    torch.cuda.synchronize(dev)
+
+    def one(t):
+        i = t % 2
+        s = streams[i]
+        with torch.cuda.stream(s):
+            dev_poses[i].copy_(host_poses[i], non_blocking=True)
+            w.render(dev_poses[i], t, out_obs=dev_obs[i], stream=s)
+            host_obs[i].copy_(dev_obs[i], non_blocking=True)
+
+    for t in range(max(3, args.warmup)):
+        one(t)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        tdist.barrier()
+    start = torch.cuda.Event(enable_timing=True)
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    start.record(streams[0])
+    streams[1].wait_event(start)
+    K = args.steps
+    for k in range(K):
+        one(k)
+    for i in range(2):
+        ends[i].record(streams[i])
+    torch.cuda.synchronize(dev)
+    ms = max(start.elapsed_time(e) for e in ends)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(ms_t, op=tdist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    return {
+        "value": world * B * K / (ms / 1e3),
+        "unit": UNIT,
+        "h2d_bytes_per_step": int(host_poses[0].numel() * 8),
+        "d2h_bytes_per_step": int(host_obs[0].numel()),
+        "gpu_launches": K,
+        "path": "pinned host poses -> pxr_render_step (C ABI via ctypes) -> pinned host obs, "
+                "2 streams",
+    }
+
+
+# ---------------------------------------------------------------- CPU legs
+
+
+def _cpu_workload(w, sample_envs, n_pose_sets):
+    import numpy as np
+
+    poses = [w.poses(t)[:sample_envs].cpu().numpy().copy() for t in range(n_pose_sets)]
+    st = w.dist.to_host()
+    frames, starts = (w.pack.flat_frames() if w.pack is not None else (None, None))
+    return poses, {k: v[:sample_envs].copy() for k, v in st.items()}, frames, starts
+
+
+def _cpu_step(O, w, poses, st, frames, starts, t, threads):
+    """One reference-path step on the CPU oracle: render_robot_batch +
+    advance_distractors + apply_* (+ grayscale), render.py:594-623,
+    distractor.py:116-214, env.py:168-173."""
+    key_t = O.fold_in((w.master.hi, w.master.lo), t)
+    B = poses.shape[0]
+    px, dp = O.render_robot_batch(w.geom, poses, w.width, w.height, w.floor_in_background,
+                                  threads=threads)
+    if w.mode == "color":
+        bias = O.color_biases(key_t, w.env_offset, B)
+        O.apply_color_inplace(px, bias, threads=threads)
+    elif w.mode == "video":
+        st["frame_cursor"], st["direction"] = O.video_advance(
+            st["frame_cursor"], st["direction"], st["frame_count"])
+        O.apply_video_inplace(px, dp, frames, starts[st["video_index"]] + st["frame_cursor"],
+                              threads=threads)
+    return O.grayscale(px) if w.grayscale else px
+
+
+def cpu_baseline(args, w, seconds=10.0):
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as O
+
+    O.build()
+    threads = O.host_threads()
+    sample_envs = min(w.batch, 1024)
+    poses, st, frames, starts = _cpu_workload(w, sample_envs, 4)
+    _cpu_step(O, w, poses[0], st, frames, starts, 0, threads)  # warm
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        _cpu_step(O, w, poses[n % 4], st, frames, starts, n, threads)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or n >= 10000:
+            break
+    return {
+        "value": n * sample_envs / el,
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "port",
+        "sample": f"{n} steps x {sample_envs} envs of the same workload ({el:.1f} s), "
+                  "C oracle (oracle/render_oracle.c: render_robot_batch + advance_distractors "
+                  "+ apply_video/apply_color), OpenMP over envs",
+        "cpu": _cpu_model(),
+    }
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args, world, rank, local):
+    """--impl reference: the reference's CPU path (oracle port) on all host
+    cores; rank 0 only under torchrun."""
+    if rank != 0:
+        return None
+    import torch
+
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as O
+
+    from paper_2502_00021_b200.bench_support import Workload
+
+    O.build()
+    threads = O.host_threads()
+    dev = torch.device("cuda", local) if torch.cuda.is_available() else None
+    if dev is None:
+        return {"impl": "reference", "unavailable": "needs the workload's pose source (CUDA)"}
+    w = Workload(args.model, args.envs, args.mode, seed=0, grayscale=args.grayscale, device=dev)
+    sample_envs = min(w.batch, 512)
+    poses, st, frames, starts = _cpu_workload(w, sample_envs, 4)
+    for t in range(max(1, args.warmup)):
+        _cpu_step(O, w, poses[t % 4], st, frames, starts, t, threads)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        _cpu_step(O, w, poses[k % 4], st, frames, starts, k, threads)
+    el = time.perf_counter() - t0
+    value = args.steps * sample_envs / el
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64/f32 raster, u8 RGB out",
+        "data": "synthetic (same pose source and video pack as the GPU arm)",
+        "config": {"workload": f"{args.model} ({w.spec.name}), {args.envs} envs/GPU, "
+                               f"{args.mode} distractors, 84x84; each step renders a bounded "
+                               f"sample of {sample_envs} envs", "model": w.spec.name,
+                   "envs_per_gpu": args.envs, "mode": args.mode},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample_envs} envs per step, {args.steps} steps",
+                         "cpu": _cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        args.gpus = world
+    if args.impl == "reference":
+        line = run_reference(args, world, rank, local)
+    else:
+        line = run_ours(args, world, rank, local)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

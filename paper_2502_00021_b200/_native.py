@@ -1,0 +1,171 @@
+"""ctypes binding of libpxr.so (the sm_100a kernels behind include/pxr.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (``make -C
+paper_2502_00021_b200/csrc``). There is deliberately no fallback: if the
+shared object is missing, or no CUDA device is present when a kernel is
+requested, the call raises -- the hot path never silently runs on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpxr.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+PXR_OK = 0
+PXR_ERR_INVALID = 1
+PXR_ERR_CUDA = 2
+PXR_ERR_UNSUPPORTED = 3
+
+MODE_NONE, MODE_COLOR, MODE_VIDEO = 0, 1, 2
+MODES = {"none": MODE_NONE, "color": MODE_COLOR, "video": MODE_VIDEO}
+
+# Every symbol include/pxr.h declares (tests check the .so exports them all).
+EXPORTED = (
+    "pxr_abi_version", "pxr_status_string", "pxr_last_error", "pxr_floor_rays",
+    "pxr_render_step", "pxr_advance_distractors", "pxr_init_distractors",
+    "pxr_apply_color", "pxr_apply_video", "pxr_grayscale", "pxr_threefry2x64",
+    "pxr_sincosf", "pxr_pose_source", "pxr_forward_kinematics",
+)
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_u64 = ctypes.c_uint64
+
+
+class Geometry(ctypes.Structure):
+    _fields_ = [
+        ("base_verts", _vp), ("vert_link", _vp), ("triangles", _vp), ("tri_colors", _vp),
+        ("n_verts", _i32), ("n_tris", _i32), ("n_links", _i32),
+    ]
+
+
+class Camera(ctypes.Structure):
+    _fields_ = [
+        ("block", ctypes.c_float * 15), ("offset_x", ctypes.c_double),
+        ("offset_z", ctypes.c_double), ("light", ctypes.c_float * 3),
+        ("floor_rays", _vp), ("floor_separable", _i32),
+    ]
+
+
+class Distractor(ctypes.Structure):
+    _fields_ = [
+        ("mode", _i32), ("color_bias", _vp), ("video_index", _vp),
+        ("frame_cursor", _vp), ("direction", _vp), ("frame_count", _vp),
+    ]
+
+
+class VideoPackC(ctypes.Structure):
+    _fields_ = [
+        ("frames", _vp), ("starts", _vp), ("counts", _vp), ("n_videos", _i64),
+        ("n_frames", _i64), ("height", _i64), ("width", _i64),
+    ]
+
+
+class StepKeys(ctypes.Structure):
+    _fields_ = [("key_hi", _u64), ("key_lo", _u64), ("env_offset", _u64),
+                ("logical_batch", _u64)]
+
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def build(force: bool = False) -> str:
+    """Compile libpxr.so for sm_100a in-tree (nvcc cross-compiles without a GPU)."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-s", "-C", CSRC] + (["-B"] if force else []), check=True)
+    return LIB_PATH
+
+
+def lib() -> ctypes.CDLL:
+    """Load libpxr.so once; raise loudly if it was never built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C {CSRC}); "
+            "there is no CPU fallback for the render path"
+        )
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    L.pxr_abi_version.restype = _i32
+    L.pxr_abi_version.argtypes = []
+    L.pxr_status_string.restype = ctypes.c_char_p
+    L.pxr_status_string.argtypes = [_i32]
+    L.pxr_last_error.restype = ctypes.c_char_p
+    L.pxr_last_error.argtypes = []
+    L.pxr_floor_rays.restype = _i32
+    L.pxr_floor_rays.argtypes = [P(ctypes.c_float), _i64, _i64, _vp, P(_i32), _vp]
+    L.pxr_render_step.restype = _i32
+    L.pxr_render_step.argtypes = [
+        P(Geometry), P(Camera), _vp, _i64, _i64, _i64, _i32, P(Distractor), P(VideoPackC),
+        _i32, P(StepKeys), _vp, _i32, _vp, _vp, _vp,
+    ]
+    L.pxr_advance_distractors.restype = _i32
+    L.pxr_advance_distractors.argtypes = [P(Distractor), P(VideoPackC), _i64, P(StepKeys), _vp, _vp]
+    L.pxr_init_distractors.restype = _i32
+    L.pxr_init_distractors.argtypes = [P(Distractor), P(VideoPackC), _i64, _u64, _u64, _u64, _vp]
+    L.pxr_apply_color.restype = _i32
+    L.pxr_apply_color.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp]
+    L.pxr_apply_video.restype = _i32
+    L.pxr_apply_video.argtypes = [_vp, _vp, P(VideoPackC), _vp, _vp, _i64, _i64, _i64, _vp]
+    L.pxr_grayscale.restype = _i32
+    L.pxr_grayscale.argtypes = [_vp, _vp, _i64, _vp]
+    L.pxr_threefry2x64.restype = _i32
+    L.pxr_threefry2x64.argtypes = [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp]
+    L.pxr_sincosf.restype = _i32
+    L.pxr_sincosf.argtypes = [_vp, _vp, _vp, _i64, _vp]
+    L.pxr_pose_source.restype = _i32
+    L.pxr_pose_source.argtypes = [_vp, _vp, _vp, _i32, _u64, _u64, _u64, _i64, _i64, _vp, _vp]
+    L.pxr_forward_kinematics.restype = _i32
+    L.pxr_forward_kinematics.argtypes = [_vp, _vp, _vp, _i32, _i64, _vp, _vp]
+    if L.pxr_abi_version() != 1:
+        raise ImportError(f"{LIB_PATH}: ABI version {L.pxr_abi_version()} != 1")
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    """Map a pxr_status to the reference's exception convention."""
+    if status == PXR_OK:
+        return
+    msg = lib().pxr_last_error().decode(errors="replace")
+    if status == PXR_ERR_INVALID:
+        raise ValueError(msg)
+    raise NativeError(f"{lib().pxr_status_string(status).decode()}: {msg}")
+
+
+def require_cuda():
+    """The device the kernels run on; raises when there is none."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_2502_00021_b200 renders on a CUDA device (sm_100a); none is "
+            "available and there is no CPU fallback"
+        )
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a tensor (None stays NULL)."""
+    if t is None:
+        return None
+    return int(t.data_ptr())

@@ -1,0 +1,58 @@
+// Shared helpers of the libpxr translation units: status/error plumbing for
+// the C ABI and the sm_100a bulk-copy (TMA 1-D) primitives.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pxr.h"
+
+namespace pxr {
+
+void set_last_error(const char *msg);
+
+inline pxr_status set_invalid(const char *msg) {
+  set_last_error(msg);
+  return PXR_ERR_INVALID;
+}
+inline pxr_status set_unsupported(const char *msg) {
+  set_last_error(msg);
+  return PXR_ERR_UNSUPPORTED;
+}
+pxr_status set_cuda(cudaError_t e, const char *where);
+
+inline pxr_status check_launch(const char *where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda(e, where);
+  return PXR_OK;
+}
+
+// ---- TMA bulk (non-tensor) copies, shared::cta -> global -----------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Make generic-proxy smem writes visible to the async (TMA) proxy.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_store_s2g(void *gdst, const void *ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :
+               : "l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// Wait until all committed bulk stores have finished READING shared memory.
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// Wait until all committed bulk stores are complete.
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+}  // namespace pxr

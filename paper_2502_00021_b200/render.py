@@ -1,0 +1,388 @@
+"""Batched robot renderer on the B200 (host side of the render path).
+
+Mirrors ``pixelctrl.render`` (/root/reference/pkg/src/pixelctrl/render.py):
+constants (50-68), ``Mesh``/``Pose``/``Camera``/``CameraConfig``/``Frame``
+(71-130), tessellation (137-230), the tracking camera (237-279),
+``RobotGeometry`` (559-591) and ``render_robot_batch`` (594-623).
+
+What changes is where the work runs: tessellation and the camera block are
+host-side and one-time (as in the reference); every per-step array --
+poses in, pixels and depth out -- lives in HBM, and the per-env world
+transform, projection, triangle setup, z-buffered raster and shading run in
+the fused sm_100a kernel behind ``pxr_render_step`` (csrc/pxr_render.cu).
+There is no CPU path: without a CUDA device these functions raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+
+__all__ = [
+    "SKY_COLOR", "FLOOR_LIGHT", "FLOOR_DARK", "AMBIENT", "DIFFUSE", "LIGHT_DIR",
+    "LINK_PALETTE", "Mesh", "Pose", "Camera", "CameraConfig", "Frame",
+    "tessellate_capsule", "tessellate_sphere", "track_camera", "camera_basis",
+    "RobotGeometry", "RobotRenderer", "render_robot_batch",
+]
+
+SKY_COLOR = (135, 206, 235)
+FLOOR_LIGHT = (158, 158, 158)
+FLOOR_DARK = (122, 122, 122)
+AMBIENT = 0.35
+DIFFUSE = 0.65
+_l = np.array([0.3, -0.5, 0.8])
+LIGHT_DIR = tuple(_l / np.linalg.norm(_l))
+LIGHT_F32 = np.asarray(LIGHT_DIR, dtype=np.float32)
+LINK_PALETTE = (
+    (0.85, 0.30, 0.23),
+    (0.23, 0.50, 0.85),
+    (0.30, 0.75, 0.35),
+    (0.93, 0.74, 0.13),
+    (0.62, 0.40, 0.80),
+    (0.20, 0.78, 0.75),
+    (0.90, 0.50, 0.15),
+)
+
+
+@dataclass(frozen=True)
+class Mesh:
+    vertices: np.ndarray  # (V, 3) float32
+    triangles: np.ndarray  # (T, 3) int32
+    base_color: tuple
+
+
+@dataclass(frozen=True)
+class Pose:
+    x: float = 0.0
+    y: float = 0.0
+    z: float = 0.0
+    pitch: float = 0.0
+
+
+@dataclass(frozen=True)
+class Camera:
+    eye: tuple
+    target: tuple
+    up: tuple = (0.0, 0.0, 1.0)
+    vertical_fov: float = 0.9
+    near: float = 0.1
+    far: float = 50.0
+
+
+@dataclass(frozen=True)
+class CameraConfig:
+    offset: tuple = (0.0, -3.0, 1.2)
+    vertical_fov: float = 0.9
+    near: float = 0.1
+    far: float = 50.0
+
+
+@dataclass
+class Frame:
+    """Batched observation buffers in HBM (render.py:108-130).
+
+    ``pixels`` (B, H, W, 3) uint8 and ``depth`` (B, H, W) float32 are CUDA
+    tensors; +inf depth marks background.
+    """
+
+    pixels: object
+    depth: object
+
+    @classmethod
+    def allocate(cls, batch: int, height: int, width: int, device=None) -> "Frame":
+        import torch
+
+        if height < 8 or width < 8:
+            raise ValueError("frames must be at least 8x8")
+        dev = device if device is not None else _native.require_cuda()
+        return cls(
+            pixels=torch.zeros((batch, height, width, 3), dtype=torch.uint8, device=dev),
+            depth=torch.zeros((batch, height, width), dtype=torch.float32, device=dev),
+        )
+
+    @property
+    def background_mask(self):
+        import torch
+
+        return torch.isinf(self.depth)
+
+    @property
+    def batch(self) -> int:
+        return int(self.pixels.shape[0])
+
+
+# ---------------------------------------------------------------- meshes
+
+
+def tessellate_sphere(radius: float, rings: int, sectors: int) -> Mesh:
+    """UV sphere, render.py:137-168 vertex/triangle order."""
+    if radius <= 0 or rings < 2 or sectors < 3:
+        raise ValueError("sphere needs radius > 0, rings >= 2, sectors >= 3")
+    verts = [(0.0, 0.0, radius), (0.0, 0.0, -radius)]
+    for k in range(1, rings):
+        phi = math.pi * k / rings
+        sp, cp = math.sin(phi), math.cos(phi)
+        for s in range(sectors):
+            ang = 2.0 * math.pi * s / sectors
+            verts.append((radius * sp * math.cos(ang), radius * sp * math.sin(ang), radius * cp))
+
+    def ring(k, s):
+        return 2 + (k - 1) * sectors + (s % sectors)
+
+    tris = []
+    for s in range(sectors):
+        tris.append((0, ring(1, s), ring(1, s + 1)))
+        tris.append((1, ring(rings - 1, s + 1), ring(rings - 1, s)))
+    for k in range(1, rings - 1):
+        for s in range(sectors):
+            a, b, c, d = ring(k, s), ring(k, s + 1), ring(k + 1, s), ring(k + 1, s + 1)
+            tris += [(a, c, d), (a, d, b)]
+    return Mesh(np.array(verts, dtype=np.float32), np.array(tris, dtype=np.int32),
+                LINK_PALETTE[0])
+
+
+def tessellate_capsule(radius: float, length: float, rings: int = 8, sectors: int = 12,
+                       base_color=LINK_PALETTE[0]) -> Mesh:
+    """Closed capsule along local +x (render.py:171-230): poles, then each
+    cap's latitude rings from pole to seam; triangles cap 0, cap 1, barrel."""
+    if radius <= 0 or length <= 0:
+        raise ValueError("capsule needs radius > 0 and length > 0")
+    if rings < 2 or sectors < 3:
+        raise ValueError("capsule needs rings >= 2 and sectors >= 3")
+    hx = length / 2.0
+    verts = [(hx + radius, 0.0, 0.0), (-hx - radius, 0.0, 0.0)]
+    for sign in (1.0, -1.0):
+        for k in range(1, rings + 1):
+            phi = (math.pi / 2.0) * k / rings
+            for s in range(sectors):
+                ang = 2.0 * math.pi * s / sectors
+                verts.append((
+                    sign * (hx + radius * math.cos(phi)),
+                    radius * math.sin(phi) * math.cos(ang),
+                    radius * math.sin(phi) * math.sin(ang),
+                ))
+
+    def ring(side, k, s):
+        return 2 + side * rings * sectors + (k - 1) * sectors + (s % sectors)
+
+    tris = []
+    for side in (0, 1):
+        for s in range(sectors):  # pole fan, winding flipped on the second cap
+            a, b = ring(side, 1, s), ring(side, 1, s + 1)
+            tris.append((side, a, b) if side == 0 else (side, b, a))
+        for k in range(1, rings):
+            for s in range(sectors):
+                a, b = ring(side, k, s), ring(side, k, s + 1)
+                c, d = ring(side, k + 1, s), ring(side, k + 1, s + 1)
+                tris += [(a, c, d), (a, d, b)] if side == 0 else [(a, d, c), (a, b, d)]
+    for s in range(sectors):  # barrel between the two seams
+        a, b = ring(0, rings, s), ring(0, rings, s + 1)
+        c, d = ring(1, rings, s), ring(1, rings, s + 1)
+        tris += [(a, d, c), (a, b, d)]
+    return Mesh(np.array(verts, dtype=np.float32), np.array(tris, dtype=np.int32),
+                base_color)
+
+
+# ---------------------------------------------------------------- camera
+
+
+def track_camera(root_pos, config: CameraConfig = CameraConfig()) -> Camera:
+    """render.py:237-249."""
+    x, z = float(root_pos[0]), float(root_pos[1])
+    ox, oy, oz = config.offset
+    return Camera(eye=(x + ox, oy, z + oz), target=(x, 0.0, z),
+                  vertical_fov=config.vertical_fov, near=config.near, far=config.far)
+
+
+def camera_basis(camera: Camera) -> np.ndarray:
+    """15-float block [eye, right, up, fwd, tan(fov/2), near, far], built in
+    f64 and stored f32 (render.py:252-279, same validation messages)."""
+    eye = np.array(camera.eye, dtype=np.float64)
+    fwd = np.array(camera.target, dtype=np.float64) - eye
+    n = np.linalg.norm(fwd)
+    if n == 0:
+        raise ValueError("camera target coincides with eye")
+    fwd /= n
+    right = np.cross(fwd, np.array(camera.up, dtype=np.float64))
+    rn = np.linalg.norm(right)
+    if rn == 0:
+        raise ValueError("camera up is parallel to the view direction")
+    right /= rn
+    upc = np.cross(right, fwd)
+    if not 0.0 < camera.vertical_fov < math.pi:
+        raise ValueError("vertical_fov outside (0, pi)")
+    if not 0.0 < camera.near < camera.far:
+        raise ValueError("need 0 < near < far")
+    out = np.empty(15, dtype=np.float32)
+    out[0:3] = eye
+    out[3:6] = right
+    out[6:9] = upc
+    out[9:12] = fwd
+    out[12] = math.tan(camera.vertical_fov / 2.0)
+    out[13] = camera.near
+    out[14] = camera.far
+    return out
+
+
+# ---------------------------------------------------------------- geometry
+
+
+class RobotGeometry:
+    """Per-model capsule links flattened for the kernel (render.py:559-591).
+
+    Host arrays are built once (coarse capsules: rings=3, sectors=8, 96
+    triangles per link) and uploaded once per device; triangle index order
+    is the z-buffer tie-break order and is preserved exactly.
+    """
+
+    def __init__(self, lengths, radii, rings: int = 3, sectors: int = 8):
+        verts, links, tris, cols = [], [], [], []
+        base = 0
+        for i, (length, radius) in enumerate(zip(lengths, radii)):
+            color = LINK_PALETTE[i % len(LINK_PALETTE)]
+            mesh = tessellate_capsule(radius, length, rings, sectors, color)
+            v = mesh.vertices.copy()
+            v[:, 0] += np.float32(length / 2.0)  # link spans origin..tip
+            verts.append(v)
+            links.append(np.full(len(v), i, dtype=np.int32))
+            tris.append(mesh.triangles + base)
+            cols.append(np.tile(np.array(color, dtype=np.float32), (len(mesh.triangles), 1)))
+            base += len(v)
+        self.n_links = len(verts)
+        self.base_verts = np.ascontiguousarray(np.concatenate(verts), dtype=np.float32)
+        self.vert_link = np.ascontiguousarray(np.concatenate(links), dtype=np.int32)
+        self.triangles = np.ascontiguousarray(np.concatenate(tris), dtype=np.int32)
+        self.tri_colors = np.ascontiguousarray(np.concatenate(cols), dtype=np.float32)
+        self._dev = {}
+
+    @property
+    def triangle_count(self) -> int:
+        return len(self.triangles)
+
+    def device_arrays(self, device):
+        """Upload once per device; returns (tensors, pxr_geometry struct)."""
+        import torch
+
+        key = str(device)
+        if key not in self._dev:
+            t = {
+                "base_verts": torch.from_numpy(self.base_verts).to(device),
+                "vert_link": torch.from_numpy(self.vert_link).to(device),
+                "triangles": torch.from_numpy(self.triangles).to(device),
+                "tri_colors": torch.from_numpy(self.tri_colors).to(device),
+            }
+            g = _native.Geometry(
+                t["base_verts"].data_ptr(), t["vert_link"].data_ptr(),
+                t["triangles"].data_ptr(), t["tri_colors"].data_ptr(),
+                len(self.base_verts), len(self.triangles), self.n_links,
+            )
+            self._dev[key] = (t, g)
+        return self._dev[key]
+
+
+class RobotRenderer:
+    """Device-resident render setup for one (geometry, camera config, W, H):
+    uploaded mesh, the shared camera block and the exact floor ray table.
+    ``render_robot_batch`` and ``Env`` reuse one of these per configuration."""
+
+    def __init__(self, geom: RobotGeometry, cam_config: CameraConfig, width: int,
+                 height: int, device=None):
+        import torch
+
+        if width < 8 or height < 8:
+            raise ValueError("frames must be at least 8x8")
+        self.device = device if device is not None else _native.require_cuda()
+        self.geom = geom
+        self.width, self.height = int(width), int(height)
+        self.cam_config = cam_config
+        self._geom_t, self.geom_c = geom.device_arrays(self.device)
+        # render.py:607-612: orientation from the camera tracking (0, 0)
+        self.cam_block = camera_basis(track_camera((0.0, 0.0), cam_config))
+        self.floor_rays = torch.empty((self.height, self.width, 3), dtype=torch.float64,
+                                      device=self.device)
+        sep = ctypes.c_int32(0)
+        blk = (ctypes.c_float * 15)(*self.cam_block.tolist())
+        with torch.cuda.device(self.device):
+            _native.check(_native.lib().pxr_floor_rays(
+                blk, self.height, self.width, self.floor_rays.data_ptr(), ctypes.byref(sep),
+                _native.stream_ptr()))
+        self.cam_c = _native.Camera(
+            blk, float(cam_config.offset[0]), float(cam_config.offset[2]),
+            (ctypes.c_float * 3)(*LIGHT_F32.tolist()), self.floor_rays.data_ptr(),
+            int(sep.value),
+        )
+
+    def render(self, poses, *, floor_in_background: bool, dist=None, pack=None,
+               advance: bool = False, keys=None, done=None, grayscale: bool = False,
+               out_obs=None, out_depth=None, want_depth: bool = True, stream=None):
+        """One fused launch (pxr_render_step). ``poses`` (B, L, 3) f64 on the
+        device. Returns (obs, depth-or-None)."""
+        import torch
+
+        if poses.dtype != torch.float64 or poses.device.type != "cuda":
+            raise ValueError("poses must be a float64 CUDA tensor")
+        poses = poses.contiguous()
+        B = int(poses.shape[0])
+        if poses.dim() != 3 or poses.shape[1] != self.geom.n_links or poses.shape[2] != 3:
+            raise ValueError(
+                f"poses must be (batch, {self.geom.n_links}, 3), got {tuple(poses.shape)}")
+        C = 1 if grayscale else 3
+        if out_obs is None:
+            out_obs = torch.empty((B, self.height, self.width, C), dtype=torch.uint8,
+                                  device=poses.device)
+        if out_depth is None and want_depth:
+            out_depth = torch.empty((B, self.height, self.width), dtype=torch.float32,
+                                    device=poses.device)
+        dist_c = dist.c_struct() if dist is not None else _native.Distractor(_native.MODE_NONE)
+        pack_c = pack.c_struct() if pack is not None else None
+        keys_c = keys
+        done_p = _native.ptr(done)
+        st = _native.stream_ptr(stream)
+        _native.check(_native.lib().pxr_render_step(
+            ctypes.byref(self.geom_c), ctypes.byref(self.cam_c), poses.data_ptr(), B,
+            self.height, self.width, int(not floor_in_background), ctypes.byref(dist_c),
+            ctypes.byref(pack_c) if pack_c is not None else None, int(advance),
+            ctypes.byref(keys_c) if keys_c is not None else None, done_p, int(grayscale),
+            out_obs.data_ptr(), _native.ptr(out_depth), st))
+        return out_obs, out_depth
+
+
+_RENDERERS: dict = {}
+
+
+def _renderer_for(geom, cam_config, width, height, device) -> RobotRenderer:
+    key = (id(geom), cam_config, width, height, str(device))
+    r = _RENDERERS.get(key)
+    if r is None or r.geom is not geom:
+        r = RobotRenderer(geom, cam_config, width, height, device)
+        _RENDERERS[key] = r
+    return r
+
+
+def render_robot_batch(geom: RobotGeometry, poses, cam_config: CameraConfig, width: int,
+                       height: int, floor_in_background: bool, threads: int = 1,
+                       out: Frame | None = None) -> Frame:
+    """render.py:594-623 on the B200: every env's robot with its own tracking
+    camera, pixels and depth returned as CUDA tensors. ``poses`` (B, L, 3)
+    float64, a CUDA tensor or a host array (copied to the device once).
+    ``threads`` is accepted for signature parity and ignored: the CUDA grid
+    replaces the host thread pool (threading_utils.py:32-42)."""
+    import torch
+
+    dev = _native.require_cuda()
+    if width < 8 or height < 8:
+        raise ValueError("frames must be at least 8x8")
+    if not isinstance(poses, torch.Tensor):
+        poses = torch.from_numpy(np.ascontiguousarray(poses, dtype=np.float64))
+    poses = poses.to(device=dev, dtype=torch.float64)
+    r = _renderer_for(geom, cam_config, int(width), int(height), dev)
+    if out is None:
+        out = Frame.allocate(int(poses.shape[0]), int(height), int(width), device=dev)
+    r.render(poses, floor_in_background=floor_in_background, out_obs=out.pixels,
+             out_depth=out.depth)
+    return out

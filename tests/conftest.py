@@ -1,0 +1,66 @@
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(REPO, "tests", "golden")
+for p in (REPO, os.path.join(REPO, "oracle")):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+MODEL_NAMES = ("cheetah_lite", "walker_lite", "hopper_lite", "ant_lite", "humanoid_lite")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+
+
+def pytest_collection_modifyitems(config, items):
+    try:
+        import torch
+
+        have_gpu = torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        have_gpu = False
+    if have_gpu:
+        return
+    skip = pytest.mark.skip(reason="no CUDA device in this container")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)
+
+
+def golden(name):
+    with np.load(os.path.join(GOLDEN, name), allow_pickle=False) as z:
+        return {k: z[k] for k in z.files}
+
+
+def replay_meta(rec):
+    return json.loads(str(rec["meta"]))
+
+
+def spec_of(name):
+    from paper_2502_00021_b200.models import STANDIN_MODELS, builtin_model, load_model
+
+    if name in STANDIN_MODELS:
+        return load_model(STANDIN_MODELS[name])
+    return builtin_model(name)
+
+
+def geometry_of(name):
+    from paper_2502_00021_b200.models import model_kinematics
+    from paper_2502_00021_b200.render import RobotGeometry
+
+    _, _, length, radius = model_kinematics(spec_of(name))
+    return RobotGeometry(length, radius)
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    import oracle as O
+
+    O.build()
+    return O

@@ -1,0 +1,222 @@
+"""Generate the golden fixtures in tests/golden/ from the LIVE reference.
+
+Run in the build container only (the reference tree is not on GPU boxes):
+
+    PYTHONDONTWRITEBYTECODE=1 NUMBA_CACHE_DIR=/tmp/numba_cache \
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Everything here calls the reference's own public functions
+(pixelctrl.render.render_robot_batch, pixelctrl.distractor.*,
+pixelctrl.env.make_env/step, pixelctrl.prng.*); the outputs are frozen
+as .npz/.json fixtures that the CPU tests (oracle pinning) and the GPU
+parity tests compare against.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+
+import pixelctrl  # noqa: E402  (the reference, via PYTHONPATH)
+from pixelctrl import distractor as D  # noqa: E402
+from pixelctrl.env import EnvConfig, make_env, step  # noqa: E402
+from pixelctrl.models import builtin_model, load_model  # noqa: E402
+from pixelctrl.physics import forward_kinematics, model_arrays  # noqa: E402
+from pixelctrl.prng import fold_in, key_from_seed  # noqa: E402
+from pixelctrl.recorder import make_policy  # noqa: E402
+from pixelctrl.render import CameraConfig, Frame, RobotGeometry, render_robot_batch  # noqa: E402
+from pixelctrl.video_pack import VideoPack, save_video_pack  # noqa: E402
+from pixelctrl.video_tools import generate_synthetic_pack  # noqa: E402
+
+assert "/root/reference" in pixelctrl.__file__, pixelctrl.__file__
+
+MODEL_DIR = os.path.join(REPO, "paper_2502_00021_b200", "assets", "models")
+MODELS = {
+    "cheetah_lite": "cheetah_lite",
+    "walker_lite": "walker_lite",
+    "hopper_lite": "hopper_lite",
+    "ant_lite": os.path.join(MODEL_DIR, "ant_lite.model"),
+    "humanoid_lite": os.path.join(MODEL_DIR, "humanoid_lite.model"),
+}
+
+
+def spec_of(name):
+    m = MODELS[name]
+    return builtin_model(m) if not m.endswith(".model") else load_model(m)
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def geometry_fixture():
+    out = {}
+    for name in MODELS:
+        a = model_arrays(spec_of(name))
+        g = RobotGeometry(a.length, a.radius)
+        out[name] = {
+            "n_verts": int(len(g.base_verts)), "n_tris": int(len(g.triangles)),
+            "base_verts": sha(g.base_verts.astype(np.float32)),
+            "vert_link": sha(g.vert_link.astype(np.int32)),
+            "triangles": sha(g.triangles.astype(np.int32)),
+            "tri_colors": sha(g.tri_colors.astype(np.float32)),
+        }
+    with open(os.path.join(HERE, "geometry.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
+def rollout_poses(name, batch, steps, seed, every):
+    """Pose snapshots from the reference's own physics under random actions."""
+    env, state, _ = make_env(EnvConfig(model=MODELS[name], batch=batch, seed=seed, threads=8))
+    act = make_policy(f"random:{seed}", env)
+    snaps = []
+    for t in range(steps):
+        state, _ = step(env, state, act(None, t))
+        if t % every == every - 1:
+            snaps.append(forward_kinematics(env.spec, state.sys.qpos))
+    return np.stack(snaps)
+
+
+def render_fixtures():
+    rng = np.random.default_rng(7)
+    for name in MODELS:
+        spec = spec_of(name)
+        a = model_arrays(spec)
+        geom = RobotGeometry(a.length, a.radius)
+        poses = rollout_poses(name, 16, 40, seed=3, every=20)  # (2, 16, L, 3)
+        poses = poses.reshape(-1, spec.n_links, 3)
+        wild = np.zeros((8, spec.n_links, 3))  # large angles (glibc |x| >= 120 path)
+        wild[:, :, 0] = rng.uniform(-0.5, 0.5, (8, spec.n_links))
+        wild[:, :, 1] = rng.uniform(0.3, 1.2, (8, spec.n_links))
+        wild[:, :, 2] = rng.uniform(-300, 300, (8, spec.n_links))
+        poses = np.concatenate([poses, wild])
+        rec = {"poses": poses}
+        for fib in (False, True):
+            fr = render_robot_batch(geom, poses, CameraConfig(), 84, 84, fib, threads=8)
+            rec[f"pixels_fib{int(fib)}"] = fr.pixels
+            rec[f"depth_fib{int(fib)}"] = fr.depth
+        fr = render_robot_batch(geom, poses[:8], CameraConfig(), 64, 48, False, threads=8)
+        rec["pixels_64x48"] = fr.pixels
+        rec["depth_64x48"] = fr.depth
+        np.savez_compressed(os.path.join(HERE, f"render_{name}.npz"), **rec)
+
+
+def small_pack(path, seed=11, videos=3, frames=5, size=16):
+    generate_synthetic_pack(key_from_seed(seed), videos, frames, size, size, path)
+    return pixelctrl.load_video_pack(path)
+
+
+def distractor_fixtures():
+    rec = {}
+    k = key_from_seed(5)
+    s = D.init_distractors("color", None, k, 64)
+    rec["color_init_seed5_b64"] = s.color_bias
+    s2 = D.init_distractors("color", None, k, 16, env_offset=48)
+    rec["color_init_seed5_off48_b16"] = s2.color_bias
+    kt = fold_in(key_from_seed(5), 3)
+    rec["color_adv_seed5_t3_b64"] = D.advance_distractors(s, kt).color_bias
+    rec["color_adv_seed5_t3_off48_b16"] = D.advance_distractors(s2, kt, env_offset=48).color_bias
+    pack_path = os.path.join("/tmp", "golden_small.pxvp")
+    pack = small_pack(pack_path)
+    frames, starts = pack.flat_frames()
+    rec["pack_frames"] = frames
+    rec["pack_starts"] = starts
+    rec["pack_counts"] = pack.frame_counts
+    v = D.init_distractors("video", pack, key_from_seed(9), 40, env_offset=3)
+    rec["video_init_seed9_off3_b40"] = v.video_index
+    seq = [v.frame_cursor.copy()]
+    dirs = [v.direction.copy()]
+    for t in range(1, 14):
+        v = D.advance_distractors(v, fold_in(key_from_seed(9), t), env_offset=3)
+        seq.append(v.frame_cursor.copy())
+        dirs.append(v.direction.copy())
+    rec["video_cursor_seq"] = np.stack(seq)
+    rec["video_dir_seq"] = np.stack(dirs)
+    # composites on a random frame with a checker background mask
+    rr = np.random.default_rng(3)
+    fr = Frame.allocate(6, 24, 20)
+    fr.pixels[:] = rr.integers(0, 256, fr.pixels.shape, dtype=np.uint8)
+    yy, xx = np.meshgrid(np.arange(24), np.arange(20), indexing="ij")
+    fr.depth[:] = np.where((yy + xx) % 3 == 0, 1.5, np.inf).astype(np.float32)
+    rec["comp_pixels"] = fr.pixels.copy()
+    rec["comp_depth"] = fr.depth.copy()
+    cs = D.init_distractors("color", None, key_from_seed(1), 6)
+    rec["comp_bias"] = cs.color_bias
+    rec["comp_color_out"] = D.apply_color(fr, cs).pixels
+    vs = D.init_distractors("video", pack, key_from_seed(2), 6)
+    vs.frame_cursor[:] = [0, 1, 2, 3, 4, 2]
+    rec["comp_vidx"] = vs.video_index
+    rec["comp_cursor"] = vs.frame_cursor
+    rec["comp_video_out"] = D.apply_video(fr, pack, vs).pixels
+    np.savez_compressed(os.path.join(HERE, "distractor.npz"), **rec)
+
+
+def replay_fixture(tag, model, batch, mode, steps, seed, observation="rgb",
+                   env_offset=0, logical_batch=None, pack_path=None):
+    """Reference env rollout: per-step poses / done flags / obs hash chain."""
+    cfg = EnvConfig(model=MODELS[model], batch=batch, seed=seed, distractor_mode=mode,
+                    video_pack_path=pack_path, observation=observation, threads=8,
+                    env_offset=env_offset, logical_batch=logical_batch)
+    env, state, obs = make_env(cfg)
+    act = make_policy(f"random:{seed}", env)
+    poses = [forward_kinematics(env.spec, state.sys.qpos)]
+    dones = [np.zeros(batch, dtype=bool)]
+    h = hashlib.sha256(b"\x00" * 32 + np.ascontiguousarray(obs).tobytes()).digest()
+    hashes = [np.frombuffer(h, dtype=np.uint8)]
+    first_obs = obs.copy()
+    for t in range(steps):
+        state, out = step(env, state, act(obs, t))
+        obs = out.obs
+        poses.append(forward_kinematics(env.spec, state.sys.qpos))
+        dones.append(out.done.copy())
+        h = hashlib.sha256(h + np.ascontiguousarray(obs).tobytes()).digest()
+        hashes.append(np.frombuffer(h, dtype=np.uint8))
+    rec = {
+        "poses": np.stack(poses), "done": np.stack(dones), "hashes": np.stack(hashes),
+        "first_obs": first_obs, "last_obs": obs,
+        "meta": np.array(json.dumps({
+            "model": model, "batch": batch, "mode": mode, "steps": steps, "seed": seed,
+            "observation": observation, "env_offset": env_offset,
+            "logical_batch": logical_batch if logical_batch is not None else batch,
+            "floor_in_background": cfg.resolved_floor_in_background,
+        })),
+    }
+    d = state.distractor
+    rec["final_color_bias"] = d.color_bias
+    rec["final_video_index"] = d.video_index
+    rec["final_frame_cursor"] = d.frame_cursor
+    rec["final_direction"] = d.direction
+    if pack_path is not None:
+        frames, starts = env.pack.flat_frames()
+        rec["pack_frames"] = frames
+        rec["pack_starts"] = starts
+        rec["pack_counts"] = env.pack.frame_counts
+    np.savez_compressed(os.path.join(HERE, f"replay_{tag}.npz"), **rec)
+    print(tag, "resets:", int(np.stack(dones).sum()), "final", h.hex()[:16])
+
+
+def main():
+    geometry_fixture()
+    render_fixtures()
+    distractor_fixtures()
+    pack = os.path.join("/tmp", "golden_replay.pxvp")
+    small_pack(pack, seed=21, videos=4, frames=7, size=32)
+    # BASELINE config 1: HalfCheetah, 1 env, 84x84, no distractors, 1000 steps.
+    replay_fixture("cheetah_none_b1", "cheetah_lite", 1, "none", 1000, 0)
+    replay_fixture("walker_video_b8", "walker_lite", 8, "video", 150, 1, pack_path=pack)
+    replay_fixture("ant_color_b8", "ant_lite", 8, "color", 60, 2)
+    replay_fixture("humanoid_video_b8_slice", "humanoid_lite", 8, "video", 120, 4,
+                   env_offset=8, logical_batch=32, pack_path=pack)
+    replay_fixture("hopper_color_gray_b4", "hopper_lite", 4, "color", 80, 5,
+                   observation="grayscale")
+
+
+if __name__ == "__main__":
+    sys.exit(main())

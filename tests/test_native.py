@@ -1,0 +1,98 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU and exports
+every entry point include/pxr.h declares; argument validation happens before
+any CUDA call (reference convention: ValueError before any kernel runs)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import REPO
+
+HEADER = os.path.join(REPO, "include", "pxr.h")
+
+
+def declared_symbols():
+    with open(HEADER) as f:
+        src = f.read()
+    return sorted(set(re.findall(r"^\s*(?:pxr_status|int32_t|const char \*)\s*(pxr_\w+)\(",
+                                 src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def native():
+    import paper_2502_00021_b200._native as N
+
+    N.build()
+    return N
+
+
+def test_header_declares_entry_points():
+    syms = declared_symbols()
+    assert "pxr_render_step" in syms and len(syms) >= 12
+
+
+def test_library_exports_every_declared_symbol(native):
+    lib = native.lib()
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    assert set(declared_symbols()) == set(native.EXPORTED)
+
+
+def test_abi_and_status_strings(native):
+    lib = native.lib()
+    assert lib.pxr_abi_version() == 1
+    assert lib.pxr_status_string(1) == b"invalid argument"
+
+
+def test_sm100a_cubin_present(native):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", native.LIB_PATH],
+                         capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out
+
+
+def test_validation_without_gpu(native):
+    lib = native.lib()
+    g = native.Geometry(None, None, None, None, 0, 0, 4)
+    cam = native.Camera()
+    d = native.Distractor(native.MODE_NONE)
+    st = lib.pxr_render_step(ctypes.byref(g), ctypes.byref(cam), None, 0, 84, 84, 0,
+                             ctypes.byref(d), None, 0, None, None, 0, None, None, None)
+    assert st == native.PXR_ERR_INVALID
+    assert b"batch" in lib.pxr_last_error()
+    st = lib.pxr_render_step(ctypes.byref(g), ctypes.byref(cam), 1, 1, 4, 84, 0,
+                             ctypes.byref(d), None, 0, None, None, 0, 1, None, None)
+    assert st == native.PXR_ERR_INVALID
+    with pytest.raises(ValueError):
+        native.check(st)
+    d = native.Distractor(7)
+    st = lib.pxr_render_step(ctypes.byref(g), ctypes.byref(cam), 1, 1, 84, 84, 0,
+                             ctypes.byref(d), None, 0, None, None, 0, 1, None, None)
+    assert st == native.PXR_ERR_INVALID
+    assert lib.pxr_apply_color(None, None, 1, 8, 8, None) == native.PXR_ERR_INVALID
+    assert lib.pxr_grayscale(None, None, 4, None) == native.PXR_ERR_INVALID
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(REPO, "paper_2502_00021_b200")
+    for root, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                with open(os.path.join(root, fn)) as f:
+                    src = f.read()
+                assert "import oracle" not in src and "oracle/" not in src.replace(
+                    "oracle/,", ""), fn
+
+
+def test_cpu_has_no_fallback(native, monkeypatch):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2502_00021_b200 as P
+
+    with pytest.raises(RuntimeError):
+        P.render_robot_batch(P.RobotGeometry([0.5], [0.05]), [[[0.0, 0.6, 0.0]]],
+                             P.CameraConfig(), 84, 84, False)

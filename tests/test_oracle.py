@@ -1,0 +1,186 @@
+"""Pin the CPU oracle (oracle/) to the reference before trusting it.
+
+Every comparison here is against fixtures frozen from the LIVE reference by
+tests/golden/make_golden.py, or against the reference's own golden vectors
+(reference tests/test_prng.py:20-74). No GPU needed.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import MODEL_NAMES, geometry_of, golden, replay_meta, spec_of
+
+# reference tests/test_prng.py:22-47
+GOLDEN_KEY_0 = (0xD2B9123EEDD0915F, 0x4831627E7DCE6036)
+GOLDEN_KEY_42 = (0xF5069347BE28EB50, 0x3306C120DCB434CC)
+GOLDEN_BITS_0 = (0x1789D6118975704B, 0x57D5674490D412BB, 0xA1997670770BE0D1, 0xAFAF98D8129F0DBB)
+GOLDEN_SPLIT_0 = (
+    (0x51D04B7680BDF9FA, 0x43C8245429F95C60),
+    (0x4541609099B34D3F, 0xC77A7A491B96E4B6),
+    (0xA6A363E1A772C828, 0x3A1FDCAE81F3E202),
+)
+GOLDEN_FOLD_0_7 = (0x68E3DF91C05D6C14, 0x741BFF0A50063A5F)
+
+
+class TestOraclePrng:
+    def test_key_from_seed(self, oracle):
+        assert oracle.key_from_seed(0) == GOLDEN_KEY_0
+        assert oracle.key_from_seed(42) == GOLDEN_KEY_42
+
+    def test_bits_split_fold(self, oracle):
+        bits = [oracle.threefry2x64(*GOLDEN_KEY_0, b, 0) for b in range(2)]
+        assert (bits[0][0], bits[0][1], bits[1][0], bits[1][1]) == GOLDEN_BITS_0
+        assert tuple(oracle.split_one(GOLDEN_KEY_0, i) for i in range(3)) == GOLDEN_SPLIT_0
+        assert oracle.fold_in(GOLDEN_KEY_0, 7) == GOLDEN_FOLD_0_7
+
+    def test_random_index(self, oracle):
+        w = oracle.threefry2x64(*GOLDEN_KEY_0, 0, 0)[0]
+        assert oracle.index_from_word(w, 1000) == 91
+
+    def test_c_threefry_matches_python(self, oracle):
+        rng = np.random.default_rng(0)
+        c0 = rng.integers(0, 2**63, 500, dtype=np.uint64)
+        y0, y1 = oracle.threefry2x64_many(GOLDEN_KEY_0[0], GOLDEN_KEY_0[1], c0, 2)
+        for i in range(0, 500, 37):
+            assert (int(y0[i]), int(y1[i])) == oracle.threefry2x64(*GOLDEN_KEY_0, int(c0[i]), 2)
+
+
+class TestOracleSinCosf:
+    def test_glibc_restatement_strided(self, oracle):
+        # The full 2^32 sweep (0 mismatches) is recorded in DESIGN.md; a
+        # strided ~1.4e8-float sweep keeps the CPU suite fast.
+        bad = oracle.lib().oracle_sincosf_selftest(0, 0xFFFFFFFF, 31)
+        assert bad == 0
+
+    def test_pitch_range_dense(self, oracle):
+        lo = np.float32(-130.0).view(np.uint32)
+        bad = oracle.lib().oracle_sincosf_selftest(0, int(np.float32(130.0).view(np.uint32)), 7)
+        assert bad == 0 and lo > 0
+
+
+class TestOracleRender:
+    @pytest.mark.parametrize("name", MODEL_NAMES)
+    def test_matches_reference_frames(self, oracle, name):
+        rec = golden(f"render_{name}.npz")
+        geom = geometry_of(name)
+        for fib in (0, 1):
+            px, dp = oracle.render_robot_batch(geom, rec["poses"], 84, 84, bool(fib), threads=4)
+            np.testing.assert_array_equal(px, rec[f"pixels_fib{fib}"])
+            np.testing.assert_array_equal(dp.view(np.uint32), rec[f"depth_fib{fib}"].view(np.uint32))
+        px, dp = oracle.render_robot_batch(geom, rec["poses"][:8], 64, 48, False, threads=2)
+        np.testing.assert_array_equal(px, rec["pixels_64x48"])
+        np.testing.assert_array_equal(dp.view(np.uint32), rec["depth_64x48"].view(np.uint32))
+
+    def test_thread_count_invariance(self, oracle):
+        rec = golden("render_walker_lite.npz")
+        geom = geometry_of("walker_lite")
+        a = oracle.render_robot_batch(geom, rec["poses"], 84, 84, False, threads=1)
+        b = oracle.render_robot_batch(geom, rec["poses"], 84, 84, False, threads=7)
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+class TestOracleDistractor:
+    def test_color_biases(self, oracle):
+        rec = golden("distractor.npz")
+        kt = oracle.fold_in(oracle.key_from_seed(5), 3)
+        np.testing.assert_array_equal(oracle.color_biases(kt, 0, 64), rec["color_adv_seed5_t3_b64"])
+        np.testing.assert_array_equal(oracle.color_biases(kt, 48, 16),
+                                      rec["color_adv_seed5_t3_off48_b16"])
+
+    def test_ping_pong(self, oracle):
+        rec = golden("distractor.npz")
+        seq, dirs = rec["video_cursor_seq"], rec["video_dir_seq"]
+        counts = rec["pack_counts"][golden("distractor.npz")["video_init_seed9_off3_b40"]]
+        c, d = seq[0], dirs[0]
+        for t in range(1, len(seq)):
+            c, d = oracle.video_advance(c, d, counts)
+            np.testing.assert_array_equal(c, seq[t])
+            np.testing.assert_array_equal(d, dirs[t])
+
+    def test_composites(self, oracle):
+        rec = golden("distractor.npz")
+        px = rec["comp_pixels"].copy()
+        oracle.apply_color_inplace(px, rec["comp_bias"])
+        np.testing.assert_array_equal(px, rec["comp_color_out"])
+        px = rec["comp_pixels"].copy()
+        fi = rec["pack_starts"][rec["comp_vidx"]] + rec["comp_cursor"]
+        oracle.apply_video_inplace(px, rec["comp_depth"], rec["pack_frames"], fi)
+        np.testing.assert_array_equal(px, rec["comp_video_out"])
+
+
+REPLAYS = ("cheetah_none_b1", "walker_video_b8", "ant_color_b8",
+           "humanoid_video_b8_slice", "hopper_color_gray_b4")
+
+
+def oracle_replay(oracle, tag, steps=None):
+    """Re-derive the reference's obs hash chain from the frozen per-step
+    poses/done flags with the oracle: render + key schedule + distractor
+    state machine (env.py:176-255)."""
+    rec = golden(f"replay_{tag}.npz")
+    m = replay_meta(rec)
+    geom = geometry_of(m["model"])
+    B, off, lb = m["batch"], m["env_offset"], m["logical_batch"]
+    master = oracle.key_from_seed(m["seed"])
+    dist_key = oracle.fold_in(master, 0xD157)
+    n = rec["poses"].shape[0] if steps is None else steps + 1
+    if m["mode"] == "video":
+        frames, starts, counts = rec["pack_frames"], rec["pack_starts"], rec["pack_counts"]
+        nvid = len(counts)
+        vidx = np.array([oracle.video_index_for_key(oracle.split_one(dist_key, off + i), nvid)
+                         for i in range(B)], dtype=np.int64)
+        cur = np.zeros(B, np.int64)
+        dirs = np.ones(B, np.int8)
+    elif m["mode"] == "color":
+        keys = [oracle.split_one(dist_key, off + i) for i in range(B)]
+        bias = np.array([[oracle.index_from_word(w, 121) - 60 for w in (
+            oracle.threefry2x64(*k, 0, 0)[0], oracle.threefry2x64(*k, 0, 0)[1],
+            oracle.threefry2x64(*k, 1, 0)[0])] for k in keys], dtype=np.int16)
+    h = b"\x00" * 32
+    for t in range(n):
+        if t > 0:
+            key_t = oracle.fold_in(master, t - 1)
+            if m["mode"] == "color":
+                bias = oracle.color_biases(key_t, off, B)
+            elif m["mode"] == "video":
+                cur, dirs = oracle.video_advance(cur, dirs, counts[vidx])
+                for i in np.nonzero(rec["done"][t])[0]:
+                    r = oracle.fold_in(key_t, lb + off + int(i))
+                    vidx[i] = oracle.video_index_for_key(r, nvid)
+                    cur[i] = 0
+                    dirs[i] = 1
+        px, dp = oracle.render_robot_batch(geom, rec["poses"][t], 84, 84,
+                                           m["floor_in_background"], threads=4)
+        if m["mode"] == "color":
+            oracle.apply_color_inplace(px, bias)
+        elif m["mode"] == "video":
+            oracle.apply_video_inplace(px, dp, frames, starts[vidx] + cur)
+        obs = oracle.grayscale(px) if m["observation"] == "grayscale" else px
+        h = hashlib.sha256(h + np.ascontiguousarray(obs).tobytes()).digest()
+        assert h == rec["hashes"][t].tobytes(), f"{tag}: oracle diverges at t={t}"
+    return rec
+
+
+class TestOracleReplay:
+    @pytest.mark.parametrize("tag", REPLAYS)
+    def test_hash_chain(self, oracle, tag):
+        steps = 200 if tag == "cheetah_none_b1" else None
+        rec = oracle_replay(oracle, tag, steps)
+        assert rec["hashes"].shape[1] == 32
+
+
+def test_oracle_header_says_test_only():
+    import os
+
+    from conftest import REPO
+
+    for f in ("oracle.h", "oracle.py", "render_oracle.c", "prng_oracle.c", "sincosf_glibc.c"):
+        with open(os.path.join(REPO, "oracle", f)) as fh:
+            head = fh.read(600)
+        assert "ORACLE / TEST INFRASTRUCTURE ONLY" in head, f
+
+
+def test_spec_of_models_load():
+    for n in MODEL_NAMES:
+        assert spec_of(n).n_links >= 4
