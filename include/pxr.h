@@ -165,6 +165,11 @@ pxr_status pxr_threefry2x64(const uint64_t *k0, const uint64_t *k1, int64_t key_
                             const uint64_t *c0, const uint64_t *c1, int64_t c1_stride,
                             uint64_t *y0, uint64_t *y1, int64_t n, void *stream);
 
+/* The render kernel's exact division (reciprocal + Markstein correction)
+ * next to IEEE a / b, for the parity test. */
+pxr_status pxr_div_check(const double *a, const double *b, double *q_pre, double *q_ieee,
+                         int64_t n, void *stream);
+
 /* Device sinf/cosf (glibc 2.39 restatement) for the parity test. */
 pxr_status pxr_sincosf(const float *x, float *s, float *c, int64_t n, void *stream);
 

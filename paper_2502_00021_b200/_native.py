@@ -29,7 +29,7 @@ EXPORTED = (
     "pxr_abi_version", "pxr_status_string", "pxr_last_error", "pxr_floor_rays",
     "pxr_render_step", "pxr_advance_distractors", "pxr_init_distractors",
     "pxr_apply_color", "pxr_apply_video", "pxr_grayscale", "pxr_threefry2x64",
-    "pxr_sincosf", "pxr_pose_source", "pxr_forward_kinematics",
+    "pxr_sincosf", "pxr_pose_source", "pxr_forward_kinematics", "pxr_div_check",
 )
 
 _vp = ctypes.c_void_p
@@ -123,6 +123,8 @@ def lib() -> ctypes.CDLL:
     L.pxr_grayscale.argtypes = [_vp, _vp, _i64, _vp]
     L.pxr_threefry2x64.restype = _i32
     L.pxr_threefry2x64.argtypes = [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp]
+    L.pxr_div_check.restype = _i32
+    L.pxr_div_check.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp]
     L.pxr_sincosf.restype = _i32
     L.pxr_sincosf.argtypes = [_vp, _vp, _vp, _i64, _vp]
     L.pxr_pose_source.restype = _i32

@@ -63,6 +63,26 @@ class TestDeviceMath:
         assert np.array_equal(s.cpu().numpy().view(np.uint32), ws.view(np.uint32))
         assert np.array_equal(c.cpu().numpy().view(np.uint32), wc.view(np.uint32))
 
+    def test_exact_division(self, torch, pkg):
+        """The raster's division (per-triangle RN reciprocal + one Markstein
+        correction) must equal IEEE a / b for every operand it can see."""
+        rng = np.random.default_rng(5)
+        n = 1 << 23
+        a = rng.uniform(-1, 1, n) * np.exp2(rng.integers(-30, 30, n))
+        b = np.abs(rng.uniform(-1, 1, n)) * np.exp2(rng.integers(-30, 30, n)) + 1e-300
+        # edge-function-like operands: products/differences of f32 values
+        fa = rng.uniform(-84, 84, (3, n)).astype(np.float32).astype(np.float64)
+        a2 = fa[0] * (np.floor(fa[1]) + 0.5 - fa[2]) - fa[1] * (np.floor(fa[0]) + 0.5 - fa[2])
+        b2 = np.abs(fa[2] * fa[1]).astype(np.float32).astype(np.float64) + 2.0 ** -20
+        A = to_dev(torch, np.concatenate([a, a2, np.zeros(8)]))
+        B = to_dev(torch, np.concatenate([b, b2, np.ones(8)]))
+        q1 = torch.empty_like(A)
+        q2 = torch.empty_like(A)
+        pkg._native.check(pkg._native.lib().pxr_div_check(
+            A.data_ptr(), B.data_ptr(), q1.data_ptr(), q2.data_ptr(), A.numel(),
+            pkg._native.stream_ptr()))
+        assert torch.equal(q1.view(torch.int64), q2.view(torch.int64))
+
     def test_threefry_matches_oracle(self, torch, pkg, oracle):
         rng = np.random.default_rng(1)
         n = 1 << 16
