@@ -8,34 +8,43 @@
 //   advance_distractors + auto-reset re-draw    distractor.py:116-137, env.py:239-244
 //   _color_kernel / _video_kernel               distractor.py:140-176
 //
-// Design (B200-first):
-//   * persistent CTAs of 16 warps, one env per CTA iteration, everything
-//     for the env in shared memory (no HBM round trip between stages);
-//   * the env's video frame is fetched into shared memory by a TMA bulk
-//     copy (cp.async.bulk + mbarrier) issued at env start;
-//   * vertex phase: per-link glibc-exact cosf/sinf once per link, world
-//     transform + projection of every vertex (f32 as the reference, f64
-//     copies and 1/z for the raster);
-//   * triangle setup: liveness ballot + prefix -> compacted live-triangle
-//     records (f64 edge coefficients, exact reciprocal of the area) and a
-//     bitmask per 8x8 screen tile; bit order == triangle index order, so
-//     walking the bits reproduces the reference's sequential z-test order;
-//   * raster: a warp owns one tile at a time (heaviest tiles first); the
-//     candidate (triangle, pixel) pairs of up to 32 triangles are flat-packed
-//     across the 32 lanes (warp scan + shuffle search), each lane runs the
-//     reference's exact f64 edge / barycentric / depth arithmetic, and
-//     same-pixel fragments inside a pass are applied in triangle order with
-//     __match_any_sync rounds;
-//   * balanced flat passes for the background (sky / exact f64 floor) and
-//     the composite (video texel from shared memory or colour clamp-add,
-//     grayscale) into a shared-memory frame that one thread stores with a
-//     single TMA bulk copy, overlapped with the next env.
+// Design (B200-first). Persistent CTAs of 16 warps,
+// one env per CTA iteration, every intermediate in shared memory; every
+// phase is a flat, balanced loop over the CTA (no per-warp ownership):
+//   0. per-link glibc-exact cosf/sinf; distractor state for 32 envs at a
+//      time (one lane per env); the env's video frame is fetched into shared
+//      memory by a TMA bulk copy (cp.async.bulk + mbarrier);
+//   1. world transform + projection of every vertex (f32 like the
+//      reference; f64 copies and 1/z for the raster);
+//   2. triangle liveness (cull, area, bbox, normal), a block scan over
+//      triangles in index order -> live index + candidate offset; sky /
+//      floor background and an empty z-buffer;
+//   3. per round of live triangles (all of them at 84x84): records with f64
+//      edge coefficients and the exact reciprocal of the area, then every
+//      (triangle, bbox pixel) candidate of the round flat over the warps:
+//      the reference's exact f64 edge / barycentric / depth arithmetic;
+//      covered fragments min-reduce their f32 depth per pixel with a 32-bit
+//      shared-memory atomicMin and are kept in a fragment list;
+//   4. exact order-independent resolve of the reference's SEQUENTIAL strict
+//      z-test (render.py:452, triangles in index order, f64 z compared with
+//      the f32 z-buffer): with F = min over fragments of RN32(z) and
+//      S = {fragments with RN32(z) == F}, the sequential winner is the
+//      highest-index member of S with z < F if one exists, else -- if F is
+//      below the starting depth -- the lowest-index member of S, else the
+//      background. (D only decreases; the first member of S always writes
+//      when F < d0; later members write iff z < F; nothing outside S can.)
+//      One atomicMax over key = (z < F) ? 0x10000 + i : 0xFFFF - i encodes
+//      both cases;
+//   5. composite (video texel from shared memory or colour clamp-add,
+//      grayscale) into a shared-memory frame stored with one TMA bulk copy
+//      overlapped with the next env.
 // Compiled with -fmad=false: no FMA contraction, every f32/f64 operation
 // rounds where numba's code does. The only FMAs are the
-// explicit __fma_rn of the glibc sinf/cosf restatement and of the
-// correctly-rounded division below.
+// explicit __fma_rn of the glibc sinf/cosf restatement and of the exact
+// division below.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/pxr.h"
 #include "pxr_internal.cuh"
@@ -45,23 +54,31 @@ namespace pxr {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kTile = 8;  // 8x8 pixel tiles
 constexpr int kMaxLinks = 64;
 constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kRoundCand = 8192;  // candidates per raster round (soft cap)
+constexpr int kFragCap = 2048;    // fragment list capacity (overflow: recompute)
 
 constexpr uint32_t kSkyRGB = 135u | (206u << 8) | (235u << 16);  // render.py:50
 
-// One live triangle after setup (post-swap vertex order, render.py:381-385).
+// One live triangle of the current round (post-swap order, render.py:381-385).
 struct __align__(16) TriRec {
   double A0, B0, A1, B1, A2, B2;  // (double) of the f32 edge vectors ax_k, ay_k
   double rcp;                     // RN(1 / (double)area2), for the exact division
   double area;                    // (double)area2
   uint16_t v0, v1, v2, flags;     // vertex ids; top-left bits (render.py:431-433)
-  uint32_t rgb;                   // flat-shaded u8 colour
-  int16_t px0, px1, py0, py1;     // clamped pixel bbox (render.py:390-403)
-  uint32_t pad;
+  uint32_t rgb;                   // flat-shaded u8 colour (render.py:404-423)
+  uint32_t cand0;                 // first candidate of this triangle in the round
+  uint16_t px0, py0, bw, bh;      // clamped pixel bbox (render.py:390-403)
+  uint32_t magic;                 // ceil(2^32 / bw): candidate -> (row, col)
 };
 static_assert(sizeof(TriRec) == 96, "TriRec layout");
+
+struct Frag {
+  double z;      // f64 depth of the candidate (render.py:450-451)
+  uint32_t pix;  // y * W + x
+  uint32_t tri;  // live index within the round (== triangle order)
+};
 
 struct RenderParams {
   const float *base_verts;
@@ -95,16 +112,18 @@ struct RenderParams {
   uint8_t *out;
   float *out_depth;
   // derived on the host
-  int tiles_x, tiles_y, n_tiles;
   int cap;        // live-triangle records per raster round
-  int words;      // bitmask words per tile = cap / 32
-  int tri_words;  // ceil(nt / 32)
-  int frame_bytes, use_bulk, vec4, vframe_bytes, vframe_bulk;
+  int chunk_cap;  // chunk-owner entries (>= round candidates / 32)
+  int round_cand; // candidate budget per round (kRoundCand; test override)
+  int frag_limit; // fragment list limit (kFragCap; test override)
+  int frame_bytes, use_bulk, vframe_bytes, vframe_bulk;
+  uint32_t wmagic;  // ceil(2^32 / W): flat pixel index -> row
+  int depth_vec;    // out_depth rows of 4 pixels are 16-byte aligned
 };
 
 struct SmemLayout {
-  int link, floor, maps, vxy64, viz, vxy32, vz, world, rec, bits, tilecnt, queue, live,
-      livepfx, depth, col, gray, vframe, total;
+  int link, floor, maps, vxy64, viz, vxy32, vz, world, cnt, ids, lcp, rec, cand0, owner, frag,
+      depth, col, wkey, dec, gray, vframe, total;
 };
 
 __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -113,27 +132,35 @@ __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   SmemLayout L;
   int o = 0;
   const int npx = p.H * p.W;
-  L.link = o;    o += align_up(p.nl * 16, 16);
-  L.floor = o;   o += align_up((p.W + 2 * p.H) * 8, 16);
-  L.maps = o;    o += align_up((p.W + p.H) * 2, 16);
-  L.vxy64 = o;   o += align_up(p.nv * 16, 16);
-  L.viz = o;     o += align_up(p.nv * 8, 16);
-  L.vxy32 = o;   o += align_up(p.nv * 8, 16);
-  L.vz = o;      o += align_up(p.nv * 4, 16);
-  L.world = o;   o += align_up(p.nv * 12, 16);
-  L.rec = o;     o += p.cap * (int)sizeof(TriRec);
-  L.bits = o;    o += align_up(p.n_tiles * p.words * 4, 16);
-  L.tilecnt = o; o += align_up(p.n_tiles * 4, 16);
-  L.queue = o;   o += align_up(p.n_tiles * 2, 16);
-  L.live = o;    o += align_up(p.tri_words * 4, 16);
-  L.livepfx = o; o += align_up(p.tri_words * 4, 16);
-  L.depth = o;   o += align_up(npx * 4, 16);
-  L.col = o;     o += align_up(npx * 3, 16);
-  L.gray = o;    o += p.gray ? align_up(npx, 16) : 0;
-  L.vframe = o;  o += p.mode == PXR_MODE_VIDEO ? align_up(p.vframe_bytes, 16) : 0;
+  L.link = o;   o += align_up(p.nl * 16, 16);
+  L.floor = o;  o += align_up((p.W + 2 * p.H) * 8, 16);
+  L.maps = o;   o += align_up((p.W + p.H) * 2, 16);
+  L.vxy64 = o;  o += align_up(p.nv * 16, 16);
+  L.viz = o;    o += align_up(p.nv * 8, 16);
+  L.vxy32 = o;  o += align_up(p.nv * 8, 16);
+  L.vz = o;     o += align_up(p.nv * 4, 16);
+  L.world = o;  o += align_up(p.nv * 12, 16);
+  L.cnt = o;    o += align_up((p.nt + 1) * 4, 16);  // bbox size per triangle
+  L.ids = o;    o += align_up((p.nt + 1) * 2, 16);  // live index -> triangle
+  L.lcp = o;    o += align_up((p.nt + 1) * 4, 16);  // live index -> candidate prefix
+  L.rec = o;    o += p.cap * (int)sizeof(TriRec);
+  L.cand0 = o;  o += align_up((p.cap + 33) * 4, 16);  // first candidate per record
+  L.owner = o;  o += align_up(p.chunk_cap * 2, 16);
+  L.frag = o;   o += kFragCap * (int)sizeof(Frag);
+  L.depth = o;  o += align_up(npx * 4, 16);
+  L.col = o;    o += align_up(npx * 3, 16);
+  L.wkey = o;   o += align_up(npx * 4, 16);
+  L.dec = o;    o += align_up(npx, 16);
+  L.gray = o;   o += p.gray ? align_up(npx, 16) : 0;
+  L.vframe = o; o += p.mode == PXR_MODE_VIDEO ? align_up(p.vframe_bytes, 16) : 0;
   L.total = o;
   return L;
 }
+
+struct DistSlot {
+  int bias[3];
+  int64_t frame_idx;
+};
 
 struct EnvShared {
   uint64_t vbar;  // mbarrier for the video frame bulk load
@@ -141,13 +168,10 @@ struct EnvShared {
   int bias[3];
   int64_t frame_idx;
   int n_live;
-  int n_queue;
-  int queue_next;
-};
-
-struct DistSlot {
-  int bias[3];
-  int64_t frame_idx;
+  int round_end;
+  int n_cand;
+  int chunk_next;
+  int overflow;
 };
 
 // Per-env distractor step (writes the new state back to HBM):
@@ -157,7 +181,7 @@ struct DistSlot {
 //           reset the re-drawn video (env.py:226-244); frame index 204.
 // With advance == 0 (make_env / observe) the stored state is used as is.
 __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t env,
-                                               DistSlot &out) {
+                                                  DistSlot &out) {
   const uint64_t g = p.env_offset + (uint64_t)env;
   out.bias[0] = out.bias[1] = out.bias[2] = 0;
   out.frame_idx = 0;
@@ -202,7 +226,7 @@ __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t
 
 // Exact RN(a / b) from y = RN(1 / b): q = RN(a*y), r = a - b*q (exact with an
 // FMA), q' = RN(q + r*y) (Markstein). Checked against IEEE division by
-// tests/test_gpu_parity.py::TestDeviceMath.
+// tests/test_gpu_parity.py::TestDeviceMath::test_exact_division.
 __device__ __forceinline__ double div_rn_pre(double a, double b, double y) {
   const double q = __dmul_rn(a, y);
   const double r = __fma_rn(-b, q, a);
@@ -215,16 +239,15 @@ __device__ __forceinline__ double half_plus(int k) {
   return __dsub_rn(big, 4503599627370495.5);          // (2^52 + k) - (2^52 - 0.5)
 }
 
-// Background of one pixel: sky, or the checker floor (render.py:306-344),
-// with the row's ray (dy, dz) and t already known for the separable case.
-__device__ __forceinline__ void floor_px(const RenderParams &p, const EnvShared &es, double dx,
+// Checker floor / sky for one pixel (render.py:306-344).
+__device__ __forceinline__ void floor_px(const RenderParams &p, float ex, float ez, double dx,
                                          double dy, double dz, float &depth, uint32_t &rgb) {
   depth = __int_as_float(0x7f800000);
   rgb = kSkyRGB;
   if (dz < -1e-12) {
-    const double t = (double)(-es.ez) / dz;
+    const double t = (double)(-ez) / dz;
     if ((double)p.cam[13] <= t && t <= (double)p.cam[14]) {
-      const double wx = (double)es.ex + t * dx;
+      const double wx = (double)ex + t * dx;
       const double wy = (double)p.cam[1] + t * dy;
       const int64_t parity = ((int64_t)floor(wx) + (int64_t)floor(wy)) & 1;
       const uint32_t c = parity == 0 ? 158u : 122u;  // render.py:51-52
@@ -232,6 +255,15 @@ __device__ __forceinline__ void floor_px(const RenderParams &p, const EnvShared 
       depth = (float)t;
     }
   }
+}
+
+// World-space vertex v (render.py:470-481): f32, no FMA contraction.
+__device__ __forceinline__ float3 world_vertex(const RenderParams &p, const float4 *s_link, int v) {
+  const float4 lk = s_link[__ldg(p.vert_link + v)];
+  const float bx = __ldg(p.base_verts + 3 * v + 0);
+  const float by = __ldg(p.base_verts + 3 * v + 1);
+  const float bz = __ldg(p.base_verts + 3 * v + 2);
+  return make_float3(lk.x + bx * lk.z - bz * lk.w, by, lk.y + bx * lk.w + bz * lk.z);
 }
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -243,12 +275,54 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
+// One candidate (triangle R, its local-th bbox pixel): the reference's exact
+// coverage test and depth (render.py:437-451).
+__device__ __forceinline__ bool eval_candidate(const RenderParams &p, const TriRec &R, int local,
+                                               const double2 *s_vxy64, const double *s_viz,
+                                               uint32_t &pix, double &z) {
+  // magic == 0 encodes bw == 1 (2^32 does not fit in 32 bits)
+  const int q = R.magic == 0u ? local : (int)__umulhi((uint32_t)local, R.magic);
+  const int px = (int)R.px0 + (local - q * (int)R.bw);
+  const int py = (int)R.py0 + q;
+  pix = (uint32_t)(py * p.W + px);
+  const double2 p0 = s_vxy64[R.v0], p1 = s_vxy64[R.v1], p2 = s_vxy64[R.v2];
+  const double pcx = half_plus(px), pcy = half_plus(py);
+  const double e0 = R.A0 * (pcy - p0.y) - R.B0 * (pcx - p0.x);
+  const double e1 = R.A1 * (pcy - p1.y) - R.B1 * (pcx - p1.x);
+  const double e2 = R.A2 * (pcy - p2.y) - R.B2 * (pcx - p2.x);
+  const uint32_t fl = R.flags;
+  if ((e0 > 0.0 || (e0 == 0.0 && (fl & 1u))) && (e1 > 0.0 || (e1 == 0.0 && (fl & 2u))) &&
+      (e2 > 0.0 || (e2 == 0.0 && (fl & 4u)))) {
+    const double l0 = div_rn_pre(e1, R.area, R.rcp);
+    const double l1 = div_rn_pre(e2, R.area, R.rcp);
+    const double l2 = div_rn_pre(e0, R.area, R.rcp);
+    const double inv_z = l0 * s_viz[R.v0] + l1 * s_viz[R.v1] + l2 * s_viz[R.v2];
+    z = __drcp_rn(inv_z);
+    return true;
+  }
+  return false;
+}
+
+// Winner of a pixel after a round (see the file header), -1 = unchanged.
+__device__ __forceinline__ int resolve_winner(uint32_t key, uint8_t dec) {
+  if (key >= 0x10000u) return (int)(key - 0x10000u);
+  if (key != 0u && dec) return (int)(0xFFFFu - key);
+  return -1;
+}
+
+__device__ __forceinline__ void put_rgb(uint8_t *col, uint32_t pix, uint32_t rgb) {
+  col[3 * pix + 0] = (uint8_t)rgb;
+  col[3 * pix + 1] = (uint8_t)(rgb >> 8);
+  col[3 * pix + 2] = (uint8_t)(rgb >> 16);
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
 render_step_kernel(const RenderParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ EnvShared es;
-  __shared__ uint32_t s_magic[kTile + 1];
   __shared__ DistSlot s_dist[32];
+  __shared__ int s_scan[kWarps];
+  __shared__ int s_wcnt[kWarps];  // fragments per warp segment
   const SmemLayout L = smem_layout(p);
   float4 *s_link = reinterpret_cast<float4 *>(smem + L.link);
   double *s_floor = reinterpret_cast<double *>(smem + L.floor);
@@ -259,14 +333,18 @@ render_step_kernel(const RenderParams p) {
   float2 *s_vxy32 = reinterpret_cast<float2 *>(smem + L.vxy32);
   float *s_vz = reinterpret_cast<float *>(smem + L.vz);
   float *s_world = reinterpret_cast<float *>(smem + L.world);
+  uint32_t *s_cand0 = reinterpret_cast<uint32_t *>(smem + L.cand0);
+  uint32_t *s_cnt = reinterpret_cast<uint32_t *>(smem + L.cnt);
+  uint16_t *s_ids = reinterpret_cast<uint16_t *>(smem + L.ids);
+  uint32_t *s_lcp = reinterpret_cast<uint32_t *>(smem + L.lcp);
   TriRec *s_rec = reinterpret_cast<TriRec *>(smem + L.rec);
-  uint32_t *s_bits = reinterpret_cast<uint32_t *>(smem + L.bits);
-  uint32_t *s_tilecnt = reinterpret_cast<uint32_t *>(smem + L.tilecnt);
-  uint16_t *s_queue = reinterpret_cast<uint16_t *>(smem + L.queue);
-  uint32_t *s_live = reinterpret_cast<uint32_t *>(smem + L.live);
-  uint32_t *s_livepfx = reinterpret_cast<uint32_t *>(smem + L.livepfx);
+  uint16_t *s_owner = reinterpret_cast<uint16_t *>(smem + L.owner);
+  Frag *s_frag = reinterpret_cast<Frag *>(smem + L.frag);
   float *s_depth = reinterpret_cast<float *>(smem + L.depth);
+  uint32_t *s_dbits = reinterpret_cast<uint32_t *>(smem + L.depth);
   uint8_t *s_col = smem + L.col;
+  uint32_t *s_wkey = reinterpret_cast<uint32_t *>(smem + L.wkey);
+  uint8_t *s_dec = smem + L.dec;
   uint8_t *s_gray = smem + L.gray;
   uint8_t *s_vframe = smem + L.vframe;
   uint8_t *s_out = p.gray ? s_gray : s_col;
@@ -282,10 +360,9 @@ render_step_kernel(const RenderParams p) {
   const float fx = p.cam[9], fy = p.cam[10], fz = p.cam[11];
   const float tanf_ = p.cam[12], near_ = p.cam[13], far_ = p.cam[14];
   const float lx = p.light[0], ly = p.light[1], lz = p.light[2];
-  const int n_bits_words = p.n_tiles * p.words;
   const uint32_t lanemask_lt = (1u << lane) - 1u;
 
-  // ---- once per CTA: floor rays, NN maps, division magics, mbarrier ------
+  // ---- once per CTA: floor rays, NN maps, mbarrier -----------------------
   if (p.draw_floor && p.floor_sep) {
     for (int i = tid; i < p.W; i += kThreads) s_floor[i] = p.floor_rays[(int64_t)i * 3];
     for (int i = tid; i < p.H; i += kThreads) {
@@ -297,7 +374,6 @@ render_step_kernel(const RenderParams p) {
     for (int i = tid; i < p.H; i += kThreads) s_rowmap[i] = (uint16_t)(((int64_t)i * p.Hv) / p.H);
     for (int i = tid; i < p.W; i += kThreads) s_colmap[i] = (uint16_t)(((int64_t)i * p.Wv) / p.W);
   }
-  if (tid <= kTile) s_magic[tid] = tid == 0 ? 0u : (65536u + tid - 1) / tid;
   if (tid == 0) {
     mbar_init(&es.vbar, 1);
     fence_mbar_init();
@@ -305,9 +381,8 @@ render_step_kernel(const RenderParams p) {
   __syncthreads();
 
   uint32_t vphase = 0;
-  int local = 0;
-  for (int64_t env = blockIdx.x; env < p.batch; env += gridDim.x, local++) {
-
+  int local_env = 0;
+  for (int64_t env = blockIdx.x; env < p.batch; env += gridDim.x, local_env++) {
     // ---- phase 0: per-link trig, camera, distractor state, video fetch ---
     for (int l = tid; l < p.nl; l += kThreads) {
       const double *pp = p.poses + ((int64_t)env * p.nl + l) * 3;
@@ -318,7 +393,7 @@ render_step_kernel(const RenderParams p) {
     if (warp == kWarps - 1) {
       // Distractor state of the next 32 envs of this CTA, one lane each, in
       // lockstep (the Threefry chains then cost one env's latency per 32).
-      if (local % 32 == 0) {
+      if (local_env % 32 == 0) {
         const int64_t e2 = env + (int64_t)lane * gridDim.x;
         if (e2 < p.batch) distractor_update(p, e2, s_dist[lane]);
         __syncwarp();
@@ -327,8 +402,7 @@ render_step_kernel(const RenderParams p) {
         const double *p0 = p.poses + (int64_t)env * p.nl * 3;
         es.ex = (float)(p0[0] + p.off_x);  // render.py:611
         es.ez = (float)(p0[1] + p.off_z);  // render.py:612
-        es.queue_next = 0;
-        const DistSlot &ds = s_dist[local % 32];
+        const DistSlot &ds = s_dist[local_env % 32];
         es.bias[0] = ds.bias[0];
         es.bias[1] = ds.bias[1];
         es.bias[2] = ds.bias[2];
@@ -340,23 +414,16 @@ render_step_kernel(const RenderParams p) {
         }
       }
     }
-    for (int i = tid; i < n_bits_words; i += kThreads) s_bits[i] = 0u;
-    for (int i = tid; i < p.n_tiles; i += kThreads) s_tilecnt[i] = 0u;
     __syncthreads();
+    const float ex = es.ex, ez = es.ez;
 
     // ---- phase 1: world transform + projection (render.py:468-481, 350-363)
     for (int v = tid; v < p.nv; v += kThreads) {
-      const float4 lk = s_link[p.vert_link[v]];
-      const float bx = p.base_verts[3 * v + 0];
-      const float by = p.base_verts[3 * v + 1];
-      const float bz = p.base_verts[3 * v + 2];
-      const float wx = lk.x + bx * lk.z - bz * lk.w;
-      const float wy = by;
-      const float wz = lk.y + bx * lk.w + bz * lk.z;
-      s_world[3 * v + 0] = wx;
-      s_world[3 * v + 1] = wy;
-      s_world[3 * v + 2] = wz;
-      const float vx = wx - es.ex, vy = wy - ey, vz = wz - es.ez;
+      const float3 w = world_vertex(p, s_link, v);
+      s_world[3 * v + 0] = w.x;
+      s_world[3 * v + 1] = w.y;
+      s_world[3 * v + 2] = w.z;
+      const float vx = w.x - ex, vy = w.y - ey, vz = w.z - ez;
       const float zv = vx * fx + vy * fy + vz * fz;
       float sx = 0.0f, sy = 0.0f;
       if ((double)zv > 1e-9) {
@@ -375,46 +442,53 @@ render_step_kernel(const RenderParams p) {
     if (tid == 0 && p.use_bulk) bulk_wait_read();
     __syncthreads();
 
-    // ---- phase 2a: triangle liveness (render.py:366-403) + background ---
-    for (int base = 0; base < p.nt; base += kThreads) {
-      const int t = base + tid;
-      bool live = false;
-      if (t < p.nt) {
-        const int i0 = p.tris[3 * t + 0], i1 = p.tris[3 * t + 1], i2 = p.tris[3 * t + 2];
-        const float z0 = s_vz[i0], z1 = s_vz[i1], z2 = s_vz[i2];
-        if (!(z0 < near_ || z1 < near_ || z2 < near_) && !(z0 > far_ && z1 > far_ && z2 > far_)) {
-          const float2 a = s_vxy32[i0], b = s_vxy32[i1], c = s_vxy32[i2];
-          const float area2 = (b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x);
-          if (area2 != 0.0f) {
-            const float minx = fminf(a.x, fminf(b.x, c.x)), maxx = fmaxf(a.x, fmaxf(b.x, c.x));
-            const float miny = fminf(a.y, fminf(b.y, c.y)), maxy = fmaxf(a.y, fmaxf(b.y, c.y));
-            double bx0 = ceil((double)minx - 0.5), bx1 = floor((double)maxx - 0.5);
-            double by0 = ceil((double)miny - 0.5), by1 = floor((double)maxy - 0.5);
-            if (bx0 < 0.0) bx0 = 0.0;
-            if (by0 < 0.0) by0 = 0.0;
-            if (bx1 > (double)(p.W - 1)) bx1 = (double)(p.W - 1);
-            if (by1 > (double)(p.H - 1)) by1 = (double)(p.H - 1);
-            if (!(bx0 > bx1 || by0 > by1)) {
-              const float *w0 = s_world + 3 * i0, *w1 = s_world + 3 * i1, *w2 = s_world + 3 * i2;
-              const float e1x = w1[0] - w0[0], e1y = w1[1] - w0[1], e1z = w1[2] - w0[2];
-              const float e2x = w2[0] - w0[0], e2y = w2[1] - w0[1], e2z = w2[2] - w0[2];
-              const float nx = e1y * e2z - e1z * e2y;
-              const float ny = e1z * e2x - e1x * e2z;
-              const float nz = e1x * e2y - e1y * e2x;
-              live = !((double)sqrtf(nx * nx + ny * ny + nz * nz) < 1e-20);  // render.py:415
-            }
+    // ---- phase 2: liveness + bbox size (render.py:366-416), background --
+    for (int t = tid; t < p.nt; t += kThreads) {
+      uint32_t n = 0;
+      const int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
+                i2 = __ldg(p.tris + 3 * t + 2);
+      const float z0 = s_vz[i0], z1 = s_vz[i1], z2 = s_vz[i2];
+      if (!(z0 < near_ || z1 < near_ || z2 < near_) && !(z0 > far_ && z1 > far_ && z2 > far_)) {
+        const float2 a = s_vxy32[i0], b = s_vxy32[i1], c = s_vxy32[i2];
+        const float area2 = (b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x);
+        if (area2 != 0.0f) {
+          const float minx = fminf(a.x, fminf(b.x, c.x)), maxx = fmaxf(a.x, fmaxf(b.x, c.x));
+          const float miny = fminf(a.y, fminf(b.y, c.y)), maxy = fmaxf(a.y, fmaxf(b.y, c.y));
+          double bx0 = ceil((double)minx - 0.5), bx1 = floor((double)maxx - 0.5);
+          double by0 = ceil((double)miny - 0.5), by1 = floor((double)maxy - 0.5);
+          if (bx0 < 0.0) bx0 = 0.0;
+          if (by0 < 0.0) by0 = 0.0;
+          if (bx1 > (double)(p.W - 1)) bx1 = (double)(p.W - 1);
+          if (by1 > (double)(p.H - 1)) by1 = (double)(p.H - 1);
+          if (!(bx0 > bx1 || by0 > by1)) {
+            const float *w0 = s_world + 3 * i0, *w1 = s_world + 3 * i1, *w2 = s_world + 3 * i2;
+            const float e1x = w1[0] - w0[0], e1y = w1[1] - w0[1], e1z = w1[2] - w0[2];
+            const float e2x = w2[0] - w0[0], e2y = w2[1] - w0[1], e2z = w2[2] - w0[2];
+            const float nx = e1y * e2z - e1z * e2y;
+            const float ny = e1z * e2x - e1x * e2z;
+            const float nz = e1x * e2y - e1y * e2x;
+            if (!((double)sqrtf(nx * nx + ny * ny + nz * nz) < 1e-20))
+              n = (uint32_t)((int)(bx1 - bx0) + 1) * (uint32_t)((int)(by1 - by0) + 1);
           }
         }
       }
-      const uint32_t word = __ballot_sync(kFull, live);
-      if (lane == 0 && base + warp * 32 < p.nt) s_live[(base >> 5) + warp] = word;
+      s_cnt[t] = n;
     }
-    // background: sky / floor, and the z-buffer (render.py:306-344)
+    // background: sky / floor under an empty z-buffer (render.py:306-344)
     if (p.mode == PXR_MODE_VIDEO && !p.draw_floor) {
-      float4 *d4 = reinterpret_cast<float4 *>(s_depth);
+      // background colour is never read (every inf pixel takes the video)
       const float inf = __int_as_float(0x7f800000);
-      for (int i = tid; i < (npx >> 2); i += kThreads) d4[i] = make_float4(inf, inf, inf, inf);
-      for (int i = (npx & ~3) + tid; i < npx; i += kThreads) s_depth[i] = inf;
+      const int n4 = npx >> 2;
+      for (int i = tid; i < n4; i += kThreads) {
+        reinterpret_cast<float4 *>(s_depth)[i] = make_float4(inf, inf, inf, inf);
+        reinterpret_cast<uint4 *>(s_wkey)[i] = make_uint4(0u, 0u, 0u, 0u);
+        reinterpret_cast<uint32_t *>(s_dec)[i] = 0u;
+      }
+      for (int i = (n4 << 2) + tid; i < npx; i += kThreads) {
+        s_depth[i] = inf;
+        s_wkey[i] = 0u;
+        s_dec[i] = 0;
+      }
     } else {
       for (int i = tid; i < npx; i += kThreads) {
         const int y = i / p.W, x = i - y * p.W;
@@ -428,44 +502,83 @@ render_step_kernel(const RenderParams p) {
             const double *r = p.floor_rays + (int64_t)i * 3;
             dx = r[0]; dy = r[1]; dz = r[2];
           }
-          floor_px(p, es, dx, dy, dz, d, c);
+          floor_px(p, ex, ez, dx, dy, dz, d, c);
         }
         s_depth[i] = d;
-        s_col[3 * i + 0] = (uint8_t)c;
-        s_col[3 * i + 1] = (uint8_t)(c >> 8);
-        s_col[3 * i + 2] = (uint8_t)(c >> 16);
+        put_rgb(s_col, (uint32_t)i, c);
+        s_wkey[i] = 0u;
+        s_dec[i] = 0;
       }
     }
     __syncthreads();
-    if (warp == 0) {  // live-triangle prefix per 32-triangle word
-      int carry = 0;
-      for (int w0 = 0; w0 < p.tri_words; w0 += 32) {
-        const int w = w0 + lane;
-        const int cnt = w < p.tri_words ? __popc(s_live[w]) : 0;
-        const int incl = warp_incl_scan(cnt, lane);
-        if (w < p.tri_words) s_livepfx[w] = carry + incl - cnt;
-        carry += __shfl_sync(kFull, incl, 31);
+    // block scans over triangles in index order: live ids, candidate prefix
+    {
+      const int per = (p.nt + kThreads - 1) / kThreads;
+      const int t0 = min(tid * per, p.nt), t1 = min(t0 + per, p.nt);
+      int nlive = 0;
+      for (int t = t0; t < t1; t++) nlive += s_cnt[t] != 0u;
+      const int wincl = warp_incl_scan(nlive, lane);
+      if (lane == 31) s_scan[warp] = wincl;
+      __syncthreads();
+      if (warp == 0) {
+        const int v = lane < kWarps ? s_scan[lane] : 0;
+        const int vi = warp_incl_scan(v, lane);
+        if (lane < kWarps) s_scan[lane] = vi - v;
+        if (lane == kWarps - 1) es.n_live = vi;
       }
-      if (lane == 0) es.n_live = carry;
+      __syncthreads();
+      int li = s_scan[warp] + wincl - nlive;
+      for (int t = t0; t < t1; t++)
+        if (s_cnt[t] != 0u) s_ids[li++] = (uint16_t)t;
+      const int n_live_ = es.n_live;
+      __syncthreads();
+      const int lper = (n_live_ + kThreads - 1) / kThreads;
+      const int l0 = min(tid * lper, n_live_), l1 = min(l0 + lper, n_live_);
+      uint32_t csum = 0;
+      for (int l = l0; l < l1; l++) csum += s_cnt[s_ids[l]];
+      const int cw = warp_incl_scan((int)csum, lane);
+      if (lane == 31) s_scan[warp] = cw;
+      __syncthreads();
+      if (warp == 0) {
+        const int v = lane < kWarps ? s_scan[lane] : 0;
+        const int vi = warp_incl_scan(v, lane);
+        if (lane < kWarps) s_scan[lane] = vi - v;
+      }
+      __syncthreads();
+      uint32_t acc = (uint32_t)(s_scan[warp] + cw) - csum;
+      for (int l = l0; l < l1; l++) {
+        s_lcp[l] = acc;
+        acc += s_cnt[s_ids[l]];
+      }
+      if (tid == kThreads - 1) s_lcp[n_live_] = acc;  // last thread holds the total
     }
     __syncthreads();
     const int n_live = es.n_live;
 
-    // ---- raster rounds over live triangles in index order --------------
-    for (int r0 = 0; r0 < n_live; r0 += p.cap) {
-      if (r0 > 0) {
-        for (int i = tid; i < n_bits_words; i += kThreads) s_bits[i] = 0u;
-        for (int i = tid; i < p.n_tiles; i += kThreads) s_tilecnt[i] = 0u;
-        if (tid == 0) es.queue_next = 0;
-        __syncthreads();
+    // ---- phases 3/4: raster rounds over live triangles in index order ---
+    for (int r0 = 0; r0 < n_live;) {
+      if (tid == 0) {
+        // live [r0, r1): at most cap triangles and ~kRoundCand candidates
+        int lo = r0 + 1, hi = min(r0 + p.cap, n_live);
+        const uint32_t base = s_lcp[r0];
+        while (lo < hi) {  // largest r1 with lcp[r1] - base <= budget
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_lcp[mid] - base <= (uint32_t)p.round_cand) lo = mid; else hi = mid - 1;
+        }
+        es.round_end = lo;
+        es.n_cand = (int)(s_lcp[lo] - base);
+        es.chunk_next = 0;
+        es.overflow = 0;
       }
-      // phase 2b: records + tile binning (render.py:366-436)
-      for (int t = tid; t < p.nt; t += kThreads) {
-        const uint32_t lw = s_live[t >> 5];
-        if (!((lw >> (t & 31)) & 1u)) continue;
-        const int cidx = (int)s_livepfx[t >> 5] + __popc(lw & ((1u << (t & 31)) - 1u)) - r0;
-        if (cidx < 0 || cidx >= p.cap) continue;
-        int i0 = p.tris[3 * t + 0], i1 = p.tris[3 * t + 1], i2 = p.tris[3 * t + 2];
+      __syncthreads();
+      const int r1 = es.round_end;
+      const int n_cand = es.n_cand;
+      const uint32_t cbase = s_lcp[r0];
+      // records (render.py:366-436) + chunk owners
+      for (int li = r0 + tid; li < r1; li += kThreads) {
+        const int t = s_ids[li];
+        int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
+            i2 = __ldg(p.tris + 3 * t + 2);
         const float2 a = s_vxy32[i0];
         float2 b = s_vxy32[i1], c = s_vxy32[i2];
         float area2 = (b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x);
@@ -482,7 +595,7 @@ render_step_kernel(const RenderParams p) {
         const double shade = 0.35 + 0.65 * ndotl;
         uint32_t rgb = 0;
         for (int ch = 0; ch < 3; ch++) {
-          double v = (double)p.tri_colors[3 * t + ch] * shade * 255.0;
+          double v = (double)__ldg(p.tri_colors + 3 * t + ch) * shade * 255.0;
           if (v > 255.0) v = 255.0;
           rgb |= ((uint32_t)v & 0xffu) << (8 * ch);
         }
@@ -515,174 +628,216 @@ render_step_kernel(const RenderParams p) {
         R.v0 = (uint16_t)i0; R.v1 = (uint16_t)i1; R.v2 = (uint16_t)i2;
         R.flags = (uint16_t)fl;
         R.rgb = rgb;
-        const int ix0 = (int)bx0, ix1 = (int)bx1, iy0 = (int)by0, iy1 = (int)by1;
-        R.px0 = (int16_t)ix0; R.px1 = (int16_t)ix1; R.py0 = (int16_t)iy0; R.py1 = (int16_t)iy1;
-        R.pad = 0;
-        s_rec[cidx] = R;
-        const uint32_t bit = 1u << (cidx & 31);
-        const int word = cidx >> 5;
-        for (int ty = iy0 / kTile; ty <= iy1 / kTile; ty++)
-          for (int tx = ix0 / kTile; tx <= ix1 / kTile; tx++) {
-            const int tile = ty * p.tiles_x + tx;
-            atomicOr(&s_bits[tile * p.words + word], bit);
-            atomicAdd(&s_tilecnt[tile], 1u);
-          }
-      }
-      __syncthreads();
-      // tile queue: non-empty tiles, heaviest first (longest-processing-time)
-      if (p.n_tiles <= 512) {
-        for (int i = tid; i < p.n_tiles; i += kThreads) {
-          const uint32_t ci = s_tilecnt[i];
-          if (ci == 0) continue;
-          int rank = 0;
-          for (int j = 0; j < p.n_tiles; j++) {
-            const uint32_t cj = s_tilecnt[j];
-            rank += (cj > ci) || (cj == ci && j < i);
-          }
-          s_queue[rank] = (uint16_t)i;
-        }
-        if (warp == 0) {
-          int ne = 0;
-          for (int i = lane; i < p.n_tiles; i += 32) ne += s_tilecnt[i] != 0u;
-          for (int s = 16; s >= 1; s >>= 1) ne += __shfl_xor_sync(kFull, ne, s);
-          if (lane == 0) es.n_queue = ne;
-        }
-      } else {  // large frames: plain compaction of the non-empty tiles
-        if (tid == 0) es.n_queue = 0;
-        __syncthreads();
-        for (int i = tid; i < p.n_tiles; i += kThreads)
-          if (s_tilecnt[i] != 0u) s_queue[atomicAdd(&es.n_queue, 1)] = (uint16_t)i;
+        const uint32_t c0 = s_lcp[li] - cbase;
+        R.cand0 = c0;
+        R.px0 = (uint16_t)(int)bx0;
+        R.py0 = (uint16_t)(int)by0;
+        const int bw = (int)(bx1 - bx0) + 1, bh = (int)(by1 - by0) + 1;
+        R.bw = (uint16_t)bw;
+        R.bh = (uint16_t)bh;
+        // ceil(2^32 / bw) through a double quotient: exact for 2 <= bw <= 2^20
+        // (the true quotient's fractional part is >= 1/bw >> the 2^-21 error)
+        R.magic = bw == 1 ? 0u : (uint32_t)ceil(4294967296.0 / (double)bw);
+        s_rec[li - r0] = R;
+        s_cand0[li - r0] = c0;
+        const uint32_t c1 = c0 + (uint32_t)(bw * bh);
+        for (uint32_t k = (c0 + 31) >> 5; k <= ((c1 - 1) >> 5); k++)
+          s_owner[k] = (uint16_t)(li - r0);
       }
       __syncthreads();
 
-      // phase 3: raster. A warp owns a tile; 32 triangles (one bitmask word)
-      // per batch, their bbox-in-tile pixels flat-packed over the lanes.
-      const int n_queue = es.n_queue;
+      // candidates, flat over the warps (32 per chunk, dynamically scheduled);
+      // each warp keeps its covered fragments in its own list segment
+      const int n_chunks = (n_cand + 31) >> 5;
+      const int n_round = r1 - r0;
+      const int seg = p.frag_limit / kWarps;  // fragments per warp segment
+      Frag *my_frag = s_frag + warp * (kFragCap / kWarps);
+      int my_cnt = 0;
       while (true) {
-        int qi = 0;
-        if (lane == 0) qi = atomicAdd(&es.queue_next, 1);
-        qi = __shfl_sync(kFull, qi, 0);
-        if (qi >= n_queue) break;
-        const int tile = s_queue[qi];
-        const int ty = tile / p.tiles_x, tx = tile - ty * p.tiles_x;
-        const int xb = tx * kTile, yb = ty * kTile;
-        const uint32_t *tb = s_bits + tile * p.words;
-        for (int w = 0; w < p.words; w++) {
-          const uint32_t m = tb[w];
-          if (m == 0u) continue;
-          int n = 0;
-          uint32_t pk = 0;
-          if ((m >> lane) & 1u) {
-            const TriRec &R = s_rec[w * 32 + lane];
-            const int cx0 = max((int)R.px0, xb), cx1 = min((int)R.px1, xb + kTile - 1);
-            const int cy0 = max((int)R.py0, yb), cy1 = min((int)R.py1, yb + kTile - 1);
-            const int bw = cx1 - cx0 + 1, bh = cy1 - cy0 + 1;
-            if (bw > 0 && bh > 0) {
-              n = bw * bh;
-              pk = (uint32_t)(cx0 - xb) | ((uint32_t)(cy0 - yb) << 3) | ((uint32_t)bw << 6) |
-                   (s_magic[bw] << 16);
+        int k = 0;
+        if (lane == 0) k = atomicAdd(&es.chunk_next, 1);
+        k = __shfl_sync(kFull, k, 0);
+        if (k >= n_chunks) break;
+        const int c = k * 32 + lane;
+        // owner triangle of candidate c: the owner of the chunk's first
+        // candidate plus the triangles that start inside the chunk up to c
+        const int o0 = s_owner[k];
+        const int mi = o0 + 1 + lane;
+        uint32_t bit = 0;
+        if (mi < n_round) {
+          const int d = (int)s_cand0[mi] - k * 32;  // >= 1
+          if (d < 32) bit = 1u << d;
+        }
+        const uint32_t starts = __reduce_or_sync(kFull, bit);
+        const int j = o0 + __popc(starts & (0xFFFFFFFFu >> (31 - lane)));
+        bool cov = false;
+        uint32_t pix = 0;
+        double z = 0.0;
+        if (c < n_cand) {
+          const TriRec &R = s_rec[j];
+          cov = eval_candidate(p, R, c - (int)s_cand0[j], s_vxy64, s_viz, pix, z);
+        }
+        const uint32_t cm = __ballot_sync(kFull, cov);
+        if (cm == 0u) continue;
+        const int slot = my_cnt + __popc(cm & lanemask_lt);
+        my_cnt += __popc(cm);
+        if (cov) {
+          const uint32_t zb = __float_as_uint((float)z);
+          if (zb < atomicMin(&s_dbits[pix], zb)) s_dec[pix] = 1;
+          if (slot < seg) {
+            Frag f;
+            f.z = z;
+            f.pix = pix;
+            f.tri = (uint32_t)j;
+            my_frag[slot] = f;
+          }
+        }
+      }
+      if (lane == 0) {
+        s_wcnt[warp] = my_cnt;
+        if (my_cnt > seg) es.overflow = 1;
+      }
+      __syncthreads();
+
+      // exact sequential-order resolve (see the file header)
+      constexpr int kSeg = kFragCap / kWarps;
+      if (!es.overflow) {
+        for (int i = tid; i < kFragCap; i += kThreads) {
+          if ((i % kSeg) >= s_wcnt[i / kSeg]) continue;
+          const Frag f = s_frag[i];
+          const uint32_t F = s_dbits[f.pix];
+          if (__float_as_uint((float)f.z) == F)
+            atomicMax(&s_wkey[f.pix],
+                      f.z < (double)__uint_as_float(F) ? 0x10000u + f.tri : 0xFFFFu - f.tri);
+        }
+        __syncthreads();
+        for (int i = tid; i < kFragCap; i += kThreads) {
+          if ((i % kSeg) >= s_wcnt[i / kSeg]) continue;
+          const Frag f = s_frag[i];
+          if (resolve_winner(s_wkey[f.pix], s_dec[f.pix]) == (int)f.tri)
+            put_rgb(s_col, f.pix, s_rec[f.tri].rgb);
+        }
+        if (r1 < n_live) {
+          __syncthreads();
+          for (int i = tid; i < kFragCap; i += kThreads) {
+            if ((i % kSeg) >= s_wcnt[i / kSeg]) continue;
+            const uint32_t px = s_frag[i].pix;
+            s_wkey[px] = 0u;
+            s_dec[px] = 0;
+          }
+        }
+      } else {
+        // fragment list overflow: recompute the candidates for both passes
+        for (int pass = 0; pass < 2; pass++) {
+          for (int k = warp; k < n_chunks; k += kWarps) {
+            const int c = k * 32 + lane;
+            if (c >= n_cand) continue;
+            int j = s_owner[k];
+            while (j + 1 < n_round && s_rec[j + 1].cand0 <= (uint32_t)c) j++;
+            const TriRec &R = s_rec[j];
+            uint32_t pix;
+            double z;
+            if (!eval_candidate(p, R, c - (int)R.cand0, s_vxy64, s_viz, pix, z)) continue;
+            const uint32_t F = s_dbits[pix];
+            if (__float_as_uint((float)z) != F) continue;
+            if (pass == 0) {
+              atomicMax(&s_wkey[pix],
+                        z < (double)__uint_as_float(F) ? 0x10000u + j : 0xFFFFu - j);
+            } else if (resolve_winner(s_wkey[pix], s_dec[pix]) == j) {
+              put_rgb(s_col, pix, R.rgb);
             }
           }
-          const int incl = warp_incl_scan(n, lane);
-          const int excl = incl - n;
-          const int N = __shfl_sync(kFull, incl, 31);
-          for (int c0 = 0; c0 < N; c0 += 32) {
-            const int c = c0 + lane;
-            // owner lane: #lanes whose inclusive end <= c (branch-free search)
-            int j = 0;
-#pragma unroll
-            for (int s = 16; s >= 1; s >>= 1) {
-              const int v = __shfl_sync(kFull, incl, j + s - 1);
-              if (v <= c) j += s;
-            }
-            const int ex = __shfl_sync(kFull, excl, j);
-            const uint32_t opk = __shfl_sync(kFull, pk, j);
-            bool cov = false;
-            double zpix = 0.0;
-            uint32_t rgb = 0;
-            int pix = 0;
-            if (c < N) {
-              const int local = c - ex;
-              const int bw = (opk >> 6) & 15;
-              const int q = (int)(((uint32_t)local * (opk >> 16)) >> 16);
-              const int px = xb + (int)(opk & 7u) + (local - q * bw);
-              const int py = yb + (int)((opk >> 3) & 7u) + q;
-              pix = py * p.W + px;
-              const TriRec &R = s_rec[w * 32 + j];
-              const double2 p0 = s_vxy64[R.v0], p1 = s_vxy64[R.v1], p2 = s_vxy64[R.v2];
-              const double pcx = half_plus(px), pcy = half_plus(py);
-              // render.py:441-446, inclusive top-left rule
-              const double e0 = R.A0 * (pcy - p0.y) - R.B0 * (pcx - p0.x);
-              const double e1 = R.A1 * (pcy - p1.y) - R.B1 * (pcx - p1.x);
-              const double e2 = R.A2 * (pcy - p2.y) - R.B2 * (pcx - p2.x);
-              const uint32_t fl = R.flags;
-              if ((e0 > 0.0 || (e0 == 0.0 && (fl & 1u))) && (e1 > 0.0 || (e1 == 0.0 && (fl & 2u))) &&
-                  (e2 > 0.0 || (e2 == 0.0 && (fl & 4u)))) {
-                // render.py:447-451
-                const double l0 = div_rn_pre(e1, R.area, R.rcp);
-                const double l1 = div_rn_pre(e2, R.area, R.rcp);
-                const double l2 = div_rn_pre(e0, R.area, R.rcp);
-                const double inv_z = l0 * s_viz[R.v0] + l1 * s_viz[R.v1] + l2 * s_viz[R.v2];
-                zpix = __drcp_rn(inv_z);
-                rgb = R.rgb;
-                cov = true;
-              }
-            }
-            // apply fragments in triangle order (lane order) per pixel
-            const uint32_t cm = __ballot_sync(kFull, cov);
-            if (cm == 0u) continue;
-            const uint32_t grp = __match_any_sync(kFull, cov ? pix : -1 - lane);
-            const int rank = __popc(grp & lanemask_lt);
-            const int rounds = __reduce_max_sync(kFull, cov ? rank : 0);
-            for (int rr = 0; rr <= rounds; rr++) {
-              if (cov && rank == rr && zpix < (double)s_depth[pix]) {  // strict (render.py:452)
-                s_depth[pix] = (float)zpix;
-                s_col[3 * pix + 0] = (uint8_t)rgb;
-                s_col[3 * pix + 1] = (uint8_t)(rgb >> 8);
-                s_col[3 * pix + 2] = (uint8_t)(rgb >> 16);
-              }
-              __syncwarp();
-            }
+          __syncthreads();
+        }
+        if (r1 < n_live) {
+          for (int i = tid; i < npx; i += kThreads) {
+            s_wkey[i] = 0u;
+            s_dec[i] = 0;
           }
         }
       }
       __syncthreads();
+      r0 = r1;
     }
 
-    // ---- phase 4: composite + postprocess (distractor.py:140-176, env.py:168-173)
+    // ---- phase 5: composite + postprocess (distractor.py:140-176, env.py:168-173)
     if (p.mode == PXR_MODE_VIDEO && p.vframe_bulk) mbar_wait_parity(&es.vbar, vphase);
     const uint8_t *vsrc = p.mode == PXR_MODE_VIDEO
                               ? (p.vframe_bulk ? s_vframe
                                                : p.frames + es.frame_idx * p.vframe_bytes)
                               : nullptr;
-    for (int i = tid; i < npx; i += kThreads) {
-      const float d = s_depth[i];
-      int r = s_col[3 * i + 0], gg = s_col[3 * i + 1], b = s_col[3 * i + 2];
-      if (p.mode == PXR_MODE_VIDEO) {
-        if (isinf(d)) {
-          const int y = i / p.W, x = i - y * p.W;
-          const uint8_t *src = vsrc + ((int)s_rowmap[y] * p.Wv + (int)s_colmap[x]) * 3;
-          r = src[0];
-          gg = src[1];
-          b = src[2];
-        }
-      } else if (p.mode == PXR_MODE_COLOR) {
-        r = min(255, max(0, r + es.bias[0]));
-        gg = min(255, max(0, gg + es.bias[1]));
-        b = min(255, max(0, b + es.bias[2]));
+    // Four consecutive pixels per thread: 12 colour bytes are three aligned
+    // words; the colour bias is a per-byte saturating add/sub (__vaddus4 /
+    // __vsubus4 == clamp(v + b, 0, 255) for |b| <= 255).
+    uint32_t bpos[3] = {0u, 0u, 0u}, bneg[3] = {0u, 0u, 0u};
+    if (p.mode == PXR_MODE_COLOR) {
+      for (int byte = 0; byte < 12; byte++) {
+        const int bc = es.bias[byte % 3];
+        bpos[byte >> 2] |= (uint32_t)(bc > 0 ? bc : 0) << (8 * (byte & 3));
+        bneg[byte >> 2] |= (uint32_t)(bc < 0 ? -bc : 0) << (8 * (byte & 3));
       }
-      if (p.gray) {
-        s_gray[i] = (uint8_t)((299u * r + 587u * gg + 114u * b + 500u) / 1000u);
+    }
+    const int ngroups = npx >> 2;
+    for (int gi = tid; gi < ngroups + (npx & 3); gi += kThreads) {
+      const bool tail = gi >= ngroups;
+      const int i0 = tail ? (ngroups << 2) + (gi - ngroups) : (gi << 2);
+      const int np_ = tail ? 1 : 4;
+      float d[4];
+      uint32_t w[3];
+      if (!tail) {
+        const float4 d4 = reinterpret_cast<const float4 *>(s_depth)[gi];
+        d[0] = d4.x; d[1] = d4.y; d[2] = d4.z; d[3] = d4.w;
+        const uint32_t *c3 = reinterpret_cast<const uint32_t *>(s_col) + 3 * gi;
+        w[0] = c3[0]; w[1] = c3[1]; w[2] = c3[2];
       } else {
-        s_col[3 * i + 0] = (uint8_t)r;
-        s_col[3 * i + 1] = (uint8_t)gg;
-        s_col[3 * i + 2] = (uint8_t)b;
+        d[0] = s_depth[i0];
+        w[0] = s_col[3 * i0] | (s_col[3 * i0 + 1] << 8) | (s_col[3 * i0 + 2] << 16);
+        w[1] = w[2] = 0u;
       }
-      if (p.out_depth != nullptr) p.out_depth[(int64_t)env * npx + i] = d;
+      if (p.mode == PXR_MODE_VIDEO) {  // distractor.py:172-176
+        int y = (int)__umulhi((uint32_t)i0, p.wmagic);
+        int x = i0 - y * p.W;
+        for (int k = 0; k < np_; k++) {
+          if (isinf(d[k])) {
+            const uint8_t *src = vsrc + ((int)s_rowmap[y] * p.Wv + (int)s_colmap[x]) * 3;
+            for (int ch = 0; ch < 3; ch++) {
+              const int byte = 3 * k + ch;
+              const int wi = byte >> 2, sh = 8 * (byte & 3);
+              w[wi] = (w[wi] & ~(0xffu << sh)) | ((uint32_t)src[ch] << sh);
+            }
+          }
+          if (++x == p.W) { x = 0; y++; }
+        }
+      } else if (p.mode == PXR_MODE_COLOR) {  // distractor.py:149-161
+        for (int q = 0; q < 3; q++) w[q] = __vsubus4(__vaddus4(w[q], bpos[q]), bneg[q]);
+      }
+      if (p.gray) {  // env.py:168-173
+        uint32_t gw = 0;
+        for (int k = 0; k < np_; k++) {
+          uint32_t ch3[3];
+          for (int ch = 0; ch < 3; ch++) {
+            const int byte = 3 * k + ch;
+            ch3[ch] = (w[byte >> 2] >> (8 * (byte & 3))) & 0xffu;
+          }
+          gw |= ((299u * ch3[0] + 587u * ch3[1] + 114u * ch3[2] + 500u) / 1000u) << (8 * k);
+        }
+        if (!tail) reinterpret_cast<uint32_t *>(s_gray)[gi] = gw;
+        else s_gray[i0] = (uint8_t)gw;
+      } else if (!tail) {
+        uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
+        c3[0] = w[0]; c3[1] = w[1]; c3[2] = w[2];
+      } else {
+        put_rgb(s_col, (uint32_t)i0, w[0]);
+      }
+      if (p.out_depth != nullptr) {
+        float *dd = p.out_depth + (int64_t)env * npx + i0;
+        if (!tail && p.depth_vec) *reinterpret_cast<float4 *>(dd) = make_float4(d[0], d[1], d[2], d[3]);
+        else for (int k = 0; k < np_; k++) dd[k] = d[k];
+      }
     }
     vphase ^= 1u;
 
-    // ---- phase 5: frame -> HBM (one TMA bulk store) --------------------
+    // ---- phase 6: frame -> HBM (one TMA bulk store) --------------------
     uint8_t *gout = p.out + (int64_t)env * p.frame_bytes;
     if (p.use_bulk) {
       fence_proxy_async_smem();
@@ -785,11 +940,11 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     return set_invalid("pxr_render_step: null struct");
   if (batch < 1) return set_invalid("batch must be >= 1");
   if (height < 8 || width < 8) return set_invalid("frames must be at least 8x8");
-  if (height > 1024 || width > 1024) return set_unsupported("frames above 1024 px per side");
   if (poses == nullptr || out_obs == nullptr) return set_invalid("null poses/out_obs");
   if (geom->n_links < 1 || geom->n_links > kMaxLinks || geom->n_verts < 0 || geom->n_tris < 0)
     return set_invalid("bad geometry sizes");
-  if (geom->n_verts > 65535) return set_unsupported("more than 65535 vertices");
+  if (geom->n_verts > 65535 || geom->n_tris > 65535)
+    return set_unsupported("more than 65535 vertices or triangles");
   if (geom->n_verts > 0 && (geom->base_verts == nullptr || geom->vert_link == nullptr))
     return set_invalid("null geometry vertex arrays");
   if (geom->n_tris > 0 && (geom->triangles == nullptr || geom->tri_colors == nullptr))
@@ -857,29 +1012,40 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   p.gray = grayscale ? 1 : 0;
   p.out = out_obs;
   p.out_depth = out_depth;
-  p.tiles_x = (p.W + kTile - 1) / kTile;
-  p.tiles_y = (p.H + kTile - 1) / kTile;
-  p.n_tiles = p.tiles_x * p.tiles_y;
-  p.tri_words = (p.nt + 31) / 32;
-  if (p.tri_words < 1) p.tri_words = 1;
   const int C = p.gray ? 1 : 3;
-  p.frame_bytes = p.H * p.W * C;
-  p.vec4 = (p.W % 4) == 0;
+  const int64_t npx64 = height * width;
+  if (npx64 > (1 << 20) || height > 4096 || width > 4096)
+    return set_unsupported("frame too large");
+  p.wmagic = (uint32_t)((0x100000000ull + (uint64_t)width - 1) / (uint64_t)width);
+  p.depth_vec = out_depth != nullptr && (npx64 % 4 == 0) &&
+                ((reinterpret_cast<uintptr_t>(out_depth) & 15) == 0);
+  p.frame_bytes = (int)(npx64 * C);
   p.use_bulk = (p.frame_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(out_obs) & 15) == 0);
+  // Test hooks (tests/test_gpu_parity.py): shrink the per-round budgets so
+  // the multi-round and fragment-overflow paths run on small inputs.
+  p.round_cand = kRoundCand;
+  p.frag_limit = kFragCap;
+  int debug_cap = 0;
+  if (const char *s = getenv("PXR_DEBUG_ROUND_CAND")) p.round_cand = atoi(s) > 0 ? atoi(s) : kRoundCand;
+  if (const char *s = getenv("PXR_DEBUG_FRAG_LIMIT")) p.frag_limit = atoi(s) >= 0 ? min(atoi(s), kFragCap) : kFragCap;
+  if (const char *s = getenv("PXR_DEBUG_CAP")) debug_cap = atoi(s);
+  // one round's candidates never exceed max(round budget, one triangle's bbox)
+  p.chunk_cap = (int)((npx64 > p.round_cand ? npx64 : p.round_cand) / 32 + 2);
 
   int dev = 0;
   cudaGetDevice(&dev);
   int max_optin = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const int budget = max_optin - (int)sizeof(EnvShared) - 64 - 1024;
-  // Live-triangle capacity per raster round: all triangles if they fit,
-  // else the largest multiple of 32 that does (extra rounds handle overflow).
-  int cap = align_up(p.nt > 0 ? p.nt : 32, 32);
+  const int budget =
+      max_optin - (int)(sizeof(EnvShared) + sizeof(DistSlot) * 32 + 4 * kWarps) - 256;
+  // Live-triangle records per round: all triangles if they fit, else the
+  // largest count that does (extra rounds handle the rest exactly).
+  int cap = p.nt > 0 ? p.nt : 1;
+  if (debug_cap > 0 && debug_cap < cap) cap = debug_cap;
   for (;;) {
     p.cap = cap;
-    p.words = cap / 32;
-    if (smem_layout(p).total <= budget || cap <= 32) break;
-    cap -= 32;
+    if (smem_layout(p).total <= budget || cap <= 16) break;
+    cap = cap > 64 ? cap - 32 : cap - 8;
   }
   const int smem = smem_layout(p).total;
   if (smem > budget) return set_unsupported("frame too large for one CTA's shared memory");

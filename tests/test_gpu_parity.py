@@ -119,6 +119,27 @@ class TestRenderGolden:
         np.testing.assert_array_equal(fr.depth.cpu().numpy().view(np.uint32),
                                       rec["depth_64x48"].view(np.uint32))
 
+    @pytest.mark.parametrize("knobs", [
+        {"PXR_DEBUG_CAP": "40"},                       # many record rounds
+        {"PXR_DEBUG_ROUND_CAND": "300"},               # many candidate rounds
+        {"PXR_DEBUG_FRAG_LIMIT": "16"},                # fragment-list overflow path
+        {"PXR_DEBUG_CAP": "24", "PXR_DEBUG_FRAG_LIMIT": "0"},
+    ])
+    def test_round_and_overflow_paths_exact(self, torch, pkg, monkeypatch, knobs):
+        """The multi-round and fragment-overflow paths (only reached by large
+        meshes / frames at default budgets) forced on the golden frames."""
+        for k, v in knobs.items():
+            monkeypatch.setenv(k, v)
+        for name in ("humanoid_lite", "cheetah_lite"):
+            rec = golden(f"render_{name}.npz")
+            geom = geometry_of(name)
+            poses = to_dev(torch, rec["poses"])
+            for fib in (0, 1):
+                fr = pkg.render_robot_batch(geom, poses, pkg.CameraConfig(), 84, 84, bool(fib))
+                np.testing.assert_array_equal(fr.pixels.cpu().numpy(), rec[f"pixels_fib{fib}"])
+                np.testing.assert_array_equal(fr.depth.cpu().numpy().view(np.uint32),
+                                              rec[f"depth_fib{fib}"].view(np.uint32))
+
     def test_host_poses_accepted(self, pkg):
         rec = golden("render_hopper_lite.npz")
         fr = pkg.render_robot_batch(geometry_of("hopper_lite"), rec["poses"], pkg.CameraConfig(),
