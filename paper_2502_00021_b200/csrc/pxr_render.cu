@@ -9,39 +9,43 @@
 //   _color_kernel / _video_kernel               distractor.py:140-176
 //
 // Design (B200-first). Persistent CTAs of 16 warps,
-// one env per CTA iteration, every intermediate in shared memory; every
-// phase is a flat, balanced loop over the CTA (no per-warp ownership):
+// one env per CTA iteration, every intermediate in shared memory, every
+// phase a flat, balanced loop over the CTA:
 //   0. per-link glibc-exact cosf/sinf; distractor state for 32 envs at a
 //      time (one lane per env); the env's video frame is fetched into shared
 //      memory by a TMA bulk copy (cp.async.bulk + mbarrier);
 //   1. world transform + projection of every vertex (f32 like the
 //      reference; f64 copies and 1/z for the raster);
-//   2. triangle liveness (cull, area, bbox, normal), a block scan over
-//      triangles in index order -> live index + candidate offset; sky /
-//      floor background and an empty z-buffer;
-//   3. per round of live triangles (all of them at 84x84): records with f64
-//      edge coefficients and the exact reciprocal of the area, then every
-//      (triangle, bbox pixel) candidate of the round flat over the warps:
-//      the reference's exact f64 edge / barycentric / depth arithmetic;
+//   2. triangle liveness exactly as the reference culls (near/far, zero
+//      area, empty pixel bbox, degenerate normal); a block scan over the
+//      triangles in index order gives live index + bbox-row prefix; sky /
+//      floor background under an empty z-buffer;
+//   3. per round of live triangles (all of them at 84x84): a record per
+//      triangle (f64 edge coefficients, exact reciprocal of the area, flat
+//      colour) plus f32 line equations for conservative row spans; then the
+//      (triangle, bbox row) units, flat over the warps: each lane computes
+//      one row's conservative span, the warp expands its 32 spans into
+//      pixel candidates (warp scan + start-mask owner search) and runs the
+//      reference's exact f64 edge / barycentric / depth arithmetic on them;
 //      covered fragments min-reduce their f32 depth per pixel with a 32-bit
-//      shared-memory atomicMin and are kept in a fragment list;
+//      shared-memory atomicMin and are appended to a fragment list;
 //   4. exact order-independent resolve of the reference's SEQUENTIAL strict
 //      z-test (render.py:452, triangles in index order, f64 z compared with
 //      the f32 z-buffer): with F = min over fragments of RN32(z) and
 //      S = {fragments with RN32(z) == F}, the sequential winner is the
 //      highest-index member of S with z < F if one exists, else -- if F is
 //      below the starting depth -- the lowest-index member of S, else the
-//      background. (D only decreases; the first member of S always writes
-//      when F < d0; later members write iff z < F; nothing outside S can.)
-//      One atomicMax over key = (z < F) ? 0x10000 + i : 0xFFFF - i encodes
-//      both cases;
+//      previous content. (D only decreases; the first member of S always
+//      writes when F < d0; later members write iff z < F; nothing outside S
+//      can.) One atomicMax over key = (z < F) ? 0x10000 + i : 0xFFFF - i
+//      encodes both cases; bit 31 of the same word records F < d0;
 //   5. composite (video texel from shared memory or colour clamp-add,
 //      grayscale) into a shared-memory frame stored with one TMA bulk copy
 //      overlapped with the next env.
 // Compiled with -fmad=false: no FMA contraction, every f32/f64 operation
-// rounds where numba's code does. The only FMAs are the
-// explicit __fma_rn of the glibc sinf/cosf restatement and of the exact
-// division below.
+// rounds where numba's code does. The only FMAs are explicit
+// (__fma_rn / __fmaf_rn): the glibc sinf/cosf restatement, the exact
+// division below and the conservative span bounds (not compared bit-wise).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -56,23 +60,32 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLinks = 64;
 constexpr uint32_t kFull = 0xffffffffu;
-constexpr int kRoundCand = 8192;  // candidates per raster round (soft cap)
-constexpr int kFragCap = 2048;    // fragment list capacity (overflow: recompute)
+constexpr int kRowCap = 4096;   // bbox rows per raster round (raised to H)
+constexpr int kFragCap = 1536;  // fragment list capacity (overflow: recompute)
+constexpr uint32_t kDecBit = 0x80000000u;
 
 constexpr uint32_t kSkyRGB = 135u | (206u << 8) | (235u << 16);  // render.py:50
 
-// One live triangle of the current round (post-swap order, render.py:381-385).
+// One live triangle of the current round (post-swap order, render.py:381-385):
+// the exact-test data ...
 struct __align__(16) TriRec {
   double A0, B0, A1, B1, A2, B2;  // (double) of the f32 edge vectors ax_k, ay_k
   double rcp;                     // RN(1 / (double)area2), for the exact division
   double area;                    // (double)area2
   uint16_t v0, v1, v2, flags;     // vertex ids; top-left bits (render.py:431-433)
   uint32_t rgb;                   // flat-shaded u8 colour (render.py:404-423)
-  uint32_t cand0;                 // first candidate of this triangle in the round
-  uint16_t px0, py0, bw, bh;      // clamped pixel bbox (render.py:390-403)
-  uint32_t magic;                 // ceil(2^32 / bw): candidate -> (row, col)
+  uint32_t pad;
 };
-static_assert(sizeof(TriRec) == 96, "TriRec layout");
+static_assert(sizeof(TriRec) == 80, "TriRec layout");
+
+// ... and its conservative row-span data (see for_row_span).
+struct __align__(16) SpanRec {
+  float r[3], c0[3], addu[3], addl[3];  // x-bounds: fma(r, y, c0) + add{u,l}
+  float hsy[3], hA[3];                  // horizontal edges: row sign test
+  uint16_t px0, px1, py0, pad;
+  uint32_t row0;                        // first row unit of the triangle
+};
+static_assert(sizeof(SpanRec) == 96, "SpanRec layout");
 
 struct Frag {
   double z;      // f64 depth of the candidate (render.py:450-451)
@@ -112,18 +125,18 @@ struct RenderParams {
   uint8_t *out;
   float *out_depth;
   // derived on the host
-  int cap;        // live-triangle records per raster round
-  int chunk_cap;  // chunk-owner entries (>= round candidates / 32)
-  int round_cand; // candidate budget per round (kRoundCand; test override)
-  int frag_limit; // fragment list limit (kFragCap; test override)
+  int cap;         // live-triangle records per raster round
+  int row_cap;     // bbox rows per raster round
+  int frag_limit;  // fragment list limit (kFragCap; test override)
   int frame_bytes, use_bulk, vframe_bytes, vframe_bulk;
   uint32_t wmagic;  // ceil(2^32 / W): flat pixel index -> row
-  int depth_vec;    // out_depth rows of 4 pixels are 16-byte aligned
+  uint32_t gmagic;  // ceil(2^32 / (W / 4)): 4-pixel group -> row (W % 4 == 0)
+  int depth_vec;    // out_depth groups of 4 pixels are 16-byte aligned
 };
 
 struct SmemLayout {
-  int link, floor, maps, vxy64, viz, vxy32, vz, world, cnt, ids, lcp, rec, cand0, owner, frag,
-      depth, col, wkey, dec, gray, vframe, total;
+  int link, floor, maps, vxy64, viz, vxy32, vz, world, rows, ids, lrp, rec, span, rowner,
+      frag, depth, col, wkey, gray, vframe, total;
 };
 
 __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -134,25 +147,24 @@ __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   const int npx = p.H * p.W;
   L.link = o;   o += align_up(p.nl * 16, 16);
   L.floor = o;  o += align_up((p.W + 2 * p.H) * 8, 16);
-  L.maps = o;   o += align_up((p.W + p.H) * 2, 16);
+  L.maps = o;   o += align_up((p.W + p.H) * 4, 16);  // texel byte offsets per row / column
   L.vxy64 = o;  o += align_up(p.nv * 16, 16);
   L.viz = o;    o += align_up(p.nv * 8, 16);
   L.vxy32 = o;  o += align_up(p.nv * 8, 16);
   L.vz = o;     o += align_up(p.nv * 4, 16);
   L.world = o;  o += align_up(p.nv * 12, 16);
-  L.cnt = o;    o += align_up((p.nt + 1) * 4, 16);  // bbox size per triangle
+  L.rows = o;   o += align_up((p.nt + 1) * 2, 16);  // bbox rows per triangle (0 = dead)
   L.ids = o;    o += align_up((p.nt + 1) * 2, 16);  // live index -> triangle
-  L.lcp = o;    o += align_up((p.nt + 1) * 4, 16);  // live index -> candidate prefix
+  L.lrp = o;    o += align_up((p.nt + 1) * 4, 16);  // live index -> bbox-row prefix
   L.rec = o;    o += p.cap * (int)sizeof(TriRec);
-  L.cand0 = o;  o += align_up((p.cap + 33) * 4, 16);  // first candidate per record
-  L.owner = o;  o += align_up(p.chunk_cap * 2, 16);
+  L.span = o;   o += align_up(p.cap * (int)sizeof(SpanRec), 16);
+  L.rowner = o; o += align_up((p.row_cap / 32 + 2) * 2, 16);
   L.frag = o;   o += kFragCap * (int)sizeof(Frag);
   L.depth = o;  o += align_up(npx * 4, 16);
   L.col = o;    o += align_up(npx * 3, 16);
   L.wkey = o;   o += align_up(npx * 4, 16);
-  L.dec = o;    o += align_up(npx, 16);
   L.gray = o;   o += p.gray ? align_up(npx, 16) : 0;
-  L.vframe = o; o += p.mode == PXR_MODE_VIDEO ? align_up(p.vframe_bytes, 16) : 0;
+  L.vframe = o; o += p.mode == PXR_MODE_VIDEO ? align_up(p.vframe_bytes + 4, 16) : 0;
   L.total = o;
   return L;
 }
@@ -169,9 +181,9 @@ struct EnvShared {
   int64_t frame_idx;
   int n_live;
   int round_end;
-  int n_cand;
+  int n_rows;
   int chunk_next;
-  int overflow;
+  int n_frag;
 };
 
 // Per-env distractor step (writes the new state back to HBM):
@@ -275,16 +287,69 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
-// One candidate (triangle R, its local-th bbox pixel): the reference's exact
-// coverage test and depth (render.py:437-451).
-__device__ __forceinline__ bool eval_candidate(const RenderParams &p, const TriRec &R, int local,
-                                               const double2 *s_vxy64, const double *s_viz,
-                                               uint32_t &pix, double &z) {
-  // magic == 0 encodes bw == 1 (2^32 does not fit in 32 bits)
-  const int q = R.magic == 0u ? local : (int)__umulhi((uint32_t)local, R.magic);
-  const int px = (int)R.px0 + (local - q * (int)R.bw);
-  const int py = (int)R.py0 + q;
-  pix = (uint32_t)(py * p.W + px);
+// Span setup of one triangle. (a, b, c) is the post-swap vertex order
+// (area2 > 0): the reference covers a pixel centre (x, y) only if every
+// edge function e_k = A_k (y - s_k.y) - B_k (x - s_k.x) is >= 0 in f64
+// (render.py:441-446). For a row, edges with B_k > 0 bound x from above by
+// s_k.x + (A_k / B_k)(y - s_k.y), edges with B_k < 0 from below; with
+// B_k == 0 the f64 value RN(A_k DY) has the exact sign of A_k * dy (and
+// RN32(pcy - s.y) the exact sign of pcy - s.y), so A_k * dy < 0 empties the
+// row. A bound is evaluated in f32 as fma(r, y, s.x - r s.y); its error is a
+// few ulps of |s.x| + |r| (|s.y| + |y|), and a pixel the f64 test accepts
+// lies at most 2^-52 (|r DY| + |DX|) beyond the exact bound. The margin
+// 2^-10 px + 2^-17 (|s.x| + |r| (|s.y| + H + 1)) covers both with a wide
+// safety factor: every pixel the reference can cover lies in its row's span,
+// and the exact f64 test then decides each span pixel.
+__device__ __forceinline__ void span_setup(const float2 a, const float2 b, const float2 c,
+                                           float ymax, SpanRec &S) {
+  const float2 v[3] = {a, b, c};
+  const float inf = __int_as_float(0x7f800000);
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    const float2 s = v[k], t = v[(k + 1) % 3];
+    const float A = t.x - s.x, B = t.y - s.y;
+    S.hsy[k] = s.y;
+    S.hA[k] = B == 0.0f ? A : 0.0f;
+    if (B != 0.0f) {
+      const float r = A / B;
+      S.r[k] = r;
+      S.c0[k] = __fmaf_rn(-r, s.y, s.x);
+      const float m = 0x1p-10f + (fabsf(s.x) + fabsf(r) * (fabsf(s.y) + ymax)) * 0x1p-17f;
+      S.addu[k] = B > 0.0f ? m : inf;
+      S.addl[k] = B < 0.0f ? -m : -inf;
+    } else {
+      S.r[k] = 0.0f;
+      S.c0[k] = 0.0f;
+      S.addu[k] = inf;
+      S.addl[k] = -inf;
+    }
+  }
+}
+
+// Conservative span of one bbox row: first pixel x0 and length (0 = empty).
+__device__ __forceinline__ int row_span(const SpanRec &S, int py, int &x0) {
+  const float y = (float)py + 0.5f;
+  float lo = (float)S.px0 + 0.5f, hi = (float)S.px1 + 0.5f;
+  bool empty = false;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    const float x = __fmaf_rn(S.r[k], y, S.c0[k]);
+    hi = fminf(hi, __fadd_rn(x, S.addu[k]));  // NaN (inf - inf) is ignored
+    lo = fmaxf(lo, __fadd_rn(x, S.addl[k]));
+    const float dy = y - S.hsy[k];
+    empty |= (S.hA[k] > 0.0f && dy < 0.0f) || (S.hA[k] < 0.0f && dy > 0.0f);
+  }
+  const float xa = fmaxf(ceilf(lo - 0.5f), (float)S.px0);
+  const float xb = fminf(floorf(hi - 0.5f), (float)S.px1);
+  x0 = (int)xa;
+  return (empty || xa > xb) ? 0 : (int)xb - (int)xa + 1;
+}
+
+// One candidate pixel of triangle R: the reference's exact coverage test and
+// depth (render.py:437-451).
+__device__ __forceinline__ bool eval_exact(const TriRec &R, int px, int py,
+                                           const double2 *s_vxy64, const double *s_viz,
+                                           double &z) {
   const double2 p0 = s_vxy64[R.v0], p1 = s_vxy64[R.v1], p2 = s_vxy64[R.v2];
   const double pcx = half_plus(px), pcy = half_plus(py);
   const double e0 = R.A0 * (pcy - p0.y) - R.B0 * (pcx - p0.x);
@@ -304,9 +369,10 @@ __device__ __forceinline__ bool eval_candidate(const RenderParams &p, const TriR
 }
 
 // Winner of a pixel after a round (see the file header), -1 = unchanged.
-__device__ __forceinline__ int resolve_winner(uint32_t key, uint8_t dec) {
+__device__ __forceinline__ int resolve_winner(uint32_t word) {
+  const uint32_t key = word & ~kDecBit;
   if (key >= 0x10000u) return (int)(key - 0x10000u);
-  if (key != 0u && dec) return (int)(0xFFFFu - key);
+  if (key != 0u && (word & kDecBit)) return (int)(0xFFFFu - key);
   return -1;
 }
 
@@ -316,35 +382,48 @@ __device__ __forceinline__ void put_rgb(uint8_t *col, uint32_t pix, uint32_t rgb
   col[3 * pix + 2] = (uint8_t)(rgb >> 16);
 }
 
+// Insert 24-bit texel t as pixel k (0..3) of a 12-byte, 3-word RGB group.
+__device__ __forceinline__ void put_texel(uint32_t w[3], int k, uint32_t t) {
+  if (k == 0) {
+    w[0] = (w[0] & 0xff000000u) | t;
+  } else if (k == 1) {
+    w[0] = (w[0] & 0x00ffffffu) | (t << 24);
+    w[1] = (w[1] & 0xffff0000u) | (t >> 8);
+  } else if (k == 2) {
+    w[1] = (w[1] & 0x0000ffffu) | (t << 16);
+    w[2] = (w[2] & 0xffffff00u) | (t >> 16);
+  } else {
+    w[2] = (w[2] & 0x000000ffu) | (t << 8);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
 render_step_kernel(const RenderParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ EnvShared es;
   __shared__ DistSlot s_dist[32];
   __shared__ int s_scan[kWarps];
-  __shared__ int s_wcnt[kWarps];  // fragments per warp segment
   const SmemLayout L = smem_layout(p);
   float4 *s_link = reinterpret_cast<float4 *>(smem + L.link);
   double *s_floor = reinterpret_cast<double *>(smem + L.floor);
-  uint16_t *s_rowmap = reinterpret_cast<uint16_t *>(smem + L.maps);
-  uint16_t *s_colmap = s_rowmap + p.H;
+  uint32_t *s_rowmap = reinterpret_cast<uint32_t *>(smem + L.maps);  // rowmap[y] * Wv * 3
+  uint32_t *s_colmap = s_rowmap + p.H;                               // colmap[x] * 3
   double2 *s_vxy64 = reinterpret_cast<double2 *>(smem + L.vxy64);
   double *s_viz = reinterpret_cast<double *>(smem + L.viz);
   float2 *s_vxy32 = reinterpret_cast<float2 *>(smem + L.vxy32);
   float *s_vz = reinterpret_cast<float *>(smem + L.vz);
   float *s_world = reinterpret_cast<float *>(smem + L.world);
-  uint32_t *s_cand0 = reinterpret_cast<uint32_t *>(smem + L.cand0);
-  uint32_t *s_cnt = reinterpret_cast<uint32_t *>(smem + L.cnt);
+  uint16_t *s_rows = reinterpret_cast<uint16_t *>(smem + L.rows);
   uint16_t *s_ids = reinterpret_cast<uint16_t *>(smem + L.ids);
-  uint32_t *s_lcp = reinterpret_cast<uint32_t *>(smem + L.lcp);
+  uint32_t *s_lrp = reinterpret_cast<uint32_t *>(smem + L.lrp);
   TriRec *s_rec = reinterpret_cast<TriRec *>(smem + L.rec);
-  uint16_t *s_owner = reinterpret_cast<uint16_t *>(smem + L.owner);
+  SpanRec *s_span = reinterpret_cast<SpanRec *>(smem + L.span);
+  uint16_t *s_rowner = reinterpret_cast<uint16_t *>(smem + L.rowner);
   Frag *s_frag = reinterpret_cast<Frag *>(smem + L.frag);
   float *s_depth = reinterpret_cast<float *>(smem + L.depth);
   uint32_t *s_dbits = reinterpret_cast<uint32_t *>(smem + L.depth);
   uint8_t *s_col = smem + L.col;
   uint32_t *s_wkey = reinterpret_cast<uint32_t *>(smem + L.wkey);
-  uint8_t *s_dec = smem + L.dec;
   uint8_t *s_gray = smem + L.gray;
   uint8_t *s_vframe = smem + L.vframe;
   uint8_t *s_out = p.gray ? s_gray : s_col;
@@ -361,6 +440,7 @@ render_step_kernel(const RenderParams p) {
   const float tanf_ = p.cam[12], near_ = p.cam[13], far_ = p.cam[14];
   const float lx = p.light[0], ly = p.light[1], lz = p.light[2];
   const uint32_t lanemask_lt = (1u << lane) - 1u;
+  const uint32_t lanemask_le = 0xFFFFFFFFu >> (31 - lane);
 
   // ---- once per CTA: floor rays, NN maps, mbarrier -----------------------
   if (p.draw_floor && p.floor_sep) {
@@ -371,8 +451,10 @@ render_step_kernel(const RenderParams p) {
     }
   }
   if (p.mode == PXR_MODE_VIDEO) {  // nearest_map, distractor.py:179-181
-    for (int i = tid; i < p.H; i += kThreads) s_rowmap[i] = (uint16_t)(((int64_t)i * p.Hv) / p.H);
-    for (int i = tid; i < p.W; i += kThreads) s_colmap[i] = (uint16_t)(((int64_t)i * p.Wv) / p.W);
+    for (int i = tid; i < p.H; i += kThreads)
+      s_rowmap[i] = (uint32_t)(((int64_t)i * p.Hv) / p.H) * p.Wv * 3;
+    for (int i = tid; i < p.W; i += kThreads)
+      s_colmap[i] = (uint32_t)(((int64_t)i * p.Wv) / p.W) * 3;
   }
   if (tid == 0) {
     mbar_init(&es.vbar, 1);
@@ -442,9 +524,9 @@ render_step_kernel(const RenderParams p) {
     if (tid == 0 && p.use_bulk) bulk_wait_read();
     __syncthreads();
 
-    // ---- phase 2: liveness + bbox size (render.py:366-416), background --
+    // ---- phase 2: liveness (render.py:366-416) + background -------------
     for (int t = tid; t < p.nt; t += kThreads) {
-      uint32_t n = 0;
+      uint32_t rows = 0;
       const int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
                 i2 = __ldg(p.tris + 3 * t + 2);
       const float z0 = s_vz[i0], z1 = s_vz[i1], z2 = s_vz[i2];
@@ -468,30 +550,28 @@ render_step_kernel(const RenderParams p) {
             const float ny = e1z * e2x - e1x * e2z;
             const float nz = e1x * e2y - e1y * e2x;
             if (!((double)sqrtf(nx * nx + ny * ny + nz * nz) < 1e-20))
-              n = (uint32_t)((int)(bx1 - bx0) + 1) * (uint32_t)((int)(by1 - by0) + 1);
+              rows = (uint32_t)((int)(by1 - by0) + 1);
           }
         }
       }
-      s_cnt[t] = n;
+      s_rows[t] = (uint16_t)rows;
     }
     // background: sky / floor under an empty z-buffer (render.py:306-344)
     if (p.mode == PXR_MODE_VIDEO && !p.draw_floor) {
-      // background colour is never read (every inf pixel takes the video)
+      // the background colour is never read: every inf pixel takes the video
       const float inf = __int_as_float(0x7f800000);
       const int n4 = npx >> 2;
       for (int i = tid; i < n4; i += kThreads) {
         reinterpret_cast<float4 *>(s_depth)[i] = make_float4(inf, inf, inf, inf);
         reinterpret_cast<uint4 *>(s_wkey)[i] = make_uint4(0u, 0u, 0u, 0u);
-        reinterpret_cast<uint32_t *>(s_dec)[i] = 0u;
       }
       for (int i = (n4 << 2) + tid; i < npx; i += kThreads) {
         s_depth[i] = inf;
         s_wkey[i] = 0u;
-        s_dec[i] = 0;
       }
     } else {
       for (int i = tid; i < npx; i += kThreads) {
-        const int y = i / p.W, x = i - y * p.W;
+        const int y = (int)__umulhi((uint32_t)i, p.wmagic), x = i - y * p.W;
         float d = __int_as_float(0x7f800000);
         uint32_t c = kSkyRGB;
         if (p.draw_floor) {
@@ -507,50 +587,43 @@ render_step_kernel(const RenderParams p) {
         s_depth[i] = d;
         put_rgb(s_col, (uint32_t)i, c);
         s_wkey[i] = 0u;
-        s_dec[i] = 0;
       }
     }
     __syncthreads();
-    // block scans over triangles in index order: live ids, candidate prefix
+    // block scan over triangles in index order: live ids, bbox-row prefix
     {
       const int per = (p.nt + kThreads - 1) / kThreads;
       const int t0 = min(tid * per, p.nt), t1 = min(t0 + per, p.nt);
-      int nlive = 0;
-      for (int t = t0; t < t1; t++) nlive += s_cnt[t] != 0u;
-      const int wincl = warp_incl_scan(nlive, lane);
+      int nlive = 0, nrows = 0;
+      for (int t = t0; t < t1; t++) {
+        const int r = s_rows[t];
+        nlive += r != 0;
+        nrows += r;
+      }
+      const int packed = nlive | (nrows << 12);  // per <= 128 < 2^12 live
+      const int wincl = warp_incl_scan(packed, lane);
       if (lane == 31) s_scan[warp] = wincl;
       __syncthreads();
       if (warp == 0) {
         const int v = lane < kWarps ? s_scan[lane] : 0;
         const int vi = warp_incl_scan(v, lane);
         if (lane < kWarps) s_scan[lane] = vi - v;
-        if (lane == kWarps - 1) es.n_live = vi;
+        if (lane == kWarps - 1) es.n_live = vi & 0xfff;
       }
       __syncthreads();
-      int li = s_scan[warp] + wincl - nlive;
-      for (int t = t0; t < t1; t++)
-        if (s_cnt[t] != 0u) s_ids[li++] = (uint16_t)t;
-      const int n_live_ = es.n_live;
-      __syncthreads();
-      const int lper = (n_live_ + kThreads - 1) / kThreads;
-      const int l0 = min(tid * lper, n_live_), l1 = min(l0 + lper, n_live_);
-      uint32_t csum = 0;
-      for (int l = l0; l < l1; l++) csum += s_cnt[s_ids[l]];
-      const int cw = warp_incl_scan((int)csum, lane);
-      if (lane == 31) s_scan[warp] = cw;
-      __syncthreads();
-      if (warp == 0) {
-        const int v = lane < kWarps ? s_scan[lane] : 0;
-        const int vi = warp_incl_scan(v, lane);
-        if (lane < kWarps) s_scan[lane] = vi - v;
+      const int base = s_scan[warp] + wincl - packed;
+      int li = base & 0xfff;
+      uint32_t racc = (uint32_t)base >> 12;
+      for (int t = t0; t < t1; t++) {
+        const int r = s_rows[t];
+        if (r != 0) {
+          s_ids[li] = (uint16_t)t;
+          s_lrp[li] = racc;
+          li++;
+          racc += (uint32_t)r;
+        }
       }
-      __syncthreads();
-      uint32_t acc = (uint32_t)(s_scan[warp] + cw) - csum;
-      for (int l = l0; l < l1; l++) {
-        s_lcp[l] = acc;
-        acc += s_cnt[s_ids[l]];
-      }
-      if (tid == kThreads - 1) s_lcp[n_live_] = acc;  // last thread holds the total
+      if (tid == kThreads - 1) s_lrp[li] = racc;  // the last thread holds the totals
     }
     __syncthreads();
     const int n_live = es.n_live;
@@ -558,23 +631,25 @@ render_step_kernel(const RenderParams p) {
     // ---- phases 3/4: raster rounds over live triangles in index order ---
     for (int r0 = 0; r0 < n_live;) {
       if (tid == 0) {
-        // live [r0, r1): at most cap triangles and ~kRoundCand candidates
+        // live [r0, r1): at most cap triangles and row_cap bbox rows (a
+        // single triangle always fits: row_cap >= H)
         int lo = r0 + 1, hi = min(r0 + p.cap, n_live);
-        const uint32_t base = s_lcp[r0];
-        while (lo < hi) {  // largest r1 with lcp[r1] - base <= budget
+        const uint32_t base = s_lrp[r0];
+        while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if (s_lcp[mid] - base <= (uint32_t)p.round_cand) lo = mid; else hi = mid - 1;
+          if (s_lrp[mid] - base <= (uint32_t)p.row_cap) lo = mid; else hi = mid - 1;
         }
         es.round_end = lo;
-        es.n_cand = (int)(s_lcp[lo] - base);
+        es.n_rows = (int)(s_lrp[lo] - base);
         es.chunk_next = 0;
-        es.overflow = 0;
+        es.n_frag = 0;
       }
       __syncthreads();
       const int r1 = es.round_end;
-      const int n_cand = es.n_cand;
-      const uint32_t cbase = s_lcp[r0];
-      // records (render.py:366-436) + chunk owners
+      const int n_rows = es.n_rows;
+      const int n_round = r1 - r0;
+      const uint32_t rbase = s_lrp[r0];
+      // records (render.py:366-436), span setup, row-chunk owners
       for (int li = r0 + tid; li < r1; li += kThreads) {
         const int t = s_ids[li];
         int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
@@ -628,133 +703,149 @@ render_step_kernel(const RenderParams p) {
         R.v0 = (uint16_t)i0; R.v1 = (uint16_t)i1; R.v2 = (uint16_t)i2;
         R.flags = (uint16_t)fl;
         R.rgb = rgb;
-        const uint32_t c0 = s_lcp[li] - cbase;
-        R.cand0 = c0;
-        R.px0 = (uint16_t)(int)bx0;
-        R.py0 = (uint16_t)(int)by0;
-        const int bw = (int)(bx1 - bx0) + 1, bh = (int)(by1 - by0) + 1;
-        R.bw = (uint16_t)bw;
-        R.bh = (uint16_t)bh;
-        // ceil(2^32 / bw) through a double quotient: exact for 2 <= bw <= 2^20
-        // (the true quotient's fractional part is >= 1/bw >> the 2^-21 error)
-        R.magic = bw == 1 ? 0u : (uint32_t)ceil(4294967296.0 / (double)bw);
+        R.pad = 0;
         s_rec[li - r0] = R;
-        s_cand0[li - r0] = c0;
-        const uint32_t c1 = c0 + (uint32_t)(bw * bh);
-        for (uint32_t k = (c0 + 31) >> 5; k <= ((c1 - 1) >> 5); k++)
-          s_owner[k] = (uint16_t)(li - r0);
+        SpanRec S;
+        span_setup(a, b, c, (float)(p.H + 1), S);
+        S.px0 = (uint16_t)(int)bx0;
+        S.px1 = (uint16_t)(int)bx1;
+        S.py0 = (uint16_t)(int)by0;
+        S.pad = 0;
+        const uint32_t u0 = s_lrp[li] - rbase;
+        S.row0 = u0;
+        s_span[li - r0] = S;
+        const uint32_t u1 = u0 + (uint32_t)((int)(by1 - by0) + 1);
+        for (uint32_t k = (u0 + 31) >> 5; k <= ((u1 - 1) >> 5); k++)
+          s_rowner[k] = (uint16_t)(li - r0);
       }
       __syncthreads();
 
-      // candidates, flat over the warps (32 per chunk, dynamically scheduled);
-      // each warp keeps its covered fragments in its own list segment
-      const int n_chunks = (n_cand + 31) >> 5;
-      const int n_round = r1 - r0;
-      const int seg = p.frag_limit / kWarps;  // fragments per warp segment
-      Frag *my_frag = s_frag + warp * (kFragCap / kWarps);
-      int my_cnt = 0;
+      // (triangle, bbox row) units, 32 per chunk, chunks scheduled
+      // dynamically; each lane computes one row span, the warp expands the
+      // chunk's spans into candidates and runs the exact test on them.
+      const int n_chunks = (n_rows + 31) >> 5;
       while (true) {
         int k = 0;
         if (lane == 0) k = atomicAdd(&es.chunk_next, 1);
         k = __shfl_sync(kFull, k, 0);
         if (k >= n_chunks) break;
-        const int c = k * 32 + lane;
-        // owner triangle of candidate c: the owner of the chunk's first
-        // candidate plus the triangles that start inside the chunk up to c
-        const int o0 = s_owner[k];
+        const int u = k * 32 + lane;
+        // owner triangle of unit u: the owner of the chunk's first unit plus
+        // the triangles starting inside the chunk up to u (all have >= 1 row)
+        const int o0 = s_rowner[k];
         const int mi = o0 + 1 + lane;
         uint32_t bit = 0;
         if (mi < n_round) {
-          const int d = (int)s_cand0[mi] - k * 32;  // >= 1
+          const int d = (int)s_span[mi].row0 - k * 32;  // >= 1
           if (d < 32) bit = 1u << d;
         }
         const uint32_t starts = __reduce_or_sync(kFull, bit);
-        const int j = o0 + __popc(starts & (0xFFFFFFFFu >> (31 - lane)));
-        bool cov = false;
-        uint32_t pix = 0;
-        double z = 0.0;
-        if (c < n_cand) {
-          const TriRec &R = s_rec[j];
-          cov = eval_candidate(p, R, c - (int)s_cand0[j], s_vxy64, s_viz, pix, z);
+        const int j = o0 + __popc(starts & lanemask_le);
+        int len = 0, x0 = 0, row = 0;
+        if (u < n_rows) {
+          const SpanRec &S = s_span[j];
+          row = (int)S.py0 + (u - (int)S.row0);
+          len = row_span(S, row, x0);
         }
-        const uint32_t cm = __ballot_sync(kFull, cov);
-        if (cm == 0u) continue;
-        const int slot = my_cnt + __popc(cm & lanemask_lt);
-        my_cnt += __popc(cm);
-        if (cov) {
-          const uint32_t zb = __float_as_uint((float)z);
-          if (zb < atomicMin(&s_dbits[pix], zb)) s_dec[pix] = 1;
-          if (slot < seg) {
-            Frag f;
-            f.z = z;
-            f.pix = pix;
-            f.tri = (uint32_t)j;
-            my_frag[slot] = f;
+        // expand the 32 spans into pixel candidates
+        const int incl = warp_incl_scan(len, lane);
+        const int excl = incl - len;
+        const int N = __shfl_sync(kFull, incl, 31);
+        for (int c0 = 0; c0 < N; c0 += 32) {
+          // span lane of candidate c = c0 + lane: the number of lanes whose
+          // inclusive end is <= c (branch-free binary search over the scan)
+          const int c = c0 + lane;
+          int owner = 0;
+#pragma unroll
+          for (int s = 16; s >= 1; s >>= 1) {
+            const int v = __shfl_sync(kFull, incl, owner + s - 1);
+            if (v <= c) owner += s;
+          }
+          const int o_ex = __shfl_sync(kFull, excl, owner & 31);
+          const int o_x0 = __shfl_sync(kFull, x0, owner & 31);
+          const int o_row = __shfl_sync(kFull, row, owner & 31);
+          const int o_tri = __shfl_sync(kFull, j, owner & 31);
+          bool cov = false;
+          uint32_t pix = 0;
+          double z = 0.0;
+          if (c < N) {
+            const int px = o_x0 + (c - o_ex);
+            pix = (uint32_t)(o_row * p.W + px);
+            cov = eval_exact(s_rec[o_tri], px, o_row, s_vxy64, s_viz, z);
+          }
+          const uint32_t cm = __ballot_sync(kFull, cov);
+          if (cm == 0u) continue;
+          const int leader = __ffs(cm) - 1;
+          int slot = 0;
+          if (lane == leader) slot = atomicAdd(&es.n_frag, __popc(cm));
+          slot = __shfl_sync(kFull, slot, leader) + __popc(cm & lanemask_lt);
+          if (cov) {
+            const uint32_t zb = __float_as_uint((float)z);
+            if (zb < atomicMin(&s_dbits[pix], zb)) atomicOr(&s_wkey[pix], kDecBit);
+            if (slot < p.frag_limit) {
+              Frag f;
+              f.z = z;
+              f.pix = pix;
+              f.tri = (uint32_t)o_tri;
+              s_frag[slot] = f;
+            }
           }
         }
-      }
-      if (lane == 0) {
-        s_wcnt[warp] = my_cnt;
-        if (my_cnt > seg) es.overflow = 1;
       }
       __syncthreads();
 
       // exact sequential-order resolve (see the file header)
-      constexpr int kSeg = kFragCap / kWarps;
-      if (!es.overflow) {
-        for (int i = tid; i < kFragCap; i += kThreads) {
-          if ((i % kSeg) >= s_wcnt[i / kSeg]) continue;
+      const int n_frag = es.n_frag;
+      if (n_frag <= p.frag_limit) {
+        for (int i = tid; i < n_frag; i += kThreads) {
           const Frag f = s_frag[i];
           const uint32_t F = s_dbits[f.pix];
-          if (__float_as_uint((float)f.z) == F)
+          if (__float_as_uint((float)f.z) == F) {
+            const uint32_t hb = s_wkey[f.pix] & kDecBit;  // stable after the barrier
             atomicMax(&s_wkey[f.pix],
-                      f.z < (double)__uint_as_float(F) ? 0x10000u + f.tri : 0xFFFFu - f.tri);
+                      hb | (f.z < (double)__uint_as_float(F) ? 0x10000u + f.tri
+                                                             : 0xFFFFu - f.tri));
+          }
         }
         __syncthreads();
-        for (int i = tid; i < kFragCap; i += kThreads) {
-          if ((i % kSeg) >= s_wcnt[i / kSeg]) continue;
+        for (int i = tid; i < n_frag; i += kThreads) {
           const Frag f = s_frag[i];
-          if (resolve_winner(s_wkey[f.pix], s_dec[f.pix]) == (int)f.tri)
-            put_rgb(s_col, f.pix, s_rec[f.tri].rgb);
+          if (resolve_winner(s_wkey[f.pix]) == (int)f.tri) put_rgb(s_col, f.pix, s_rec[f.tri].rgb);
         }
         if (r1 < n_live) {
           __syncthreads();
-          for (int i = tid; i < kFragCap; i += kThreads) {
-            if ((i % kSeg) >= s_wcnt[i / kSeg]) continue;
-            const uint32_t px = s_frag[i].pix;
-            s_wkey[px] = 0u;
-            s_dec[px] = 0;
-          }
+          for (int i = tid; i < n_frag; i += kThreads) s_wkey[s_frag[i].pix] = 0u;
         }
       } else {
         // fragment list overflow: recompute the candidates for both passes
         for (int pass = 0; pass < 2; pass++) {
-          for (int k = warp; k < n_chunks; k += kWarps) {
-            const int c = k * 32 + lane;
-            if (c >= n_cand) continue;
-            int j = s_owner[k];
-            while (j + 1 < n_round && s_rec[j + 1].cand0 <= (uint32_t)c) j++;
+          for (int u = tid; u < n_rows; u += kThreads) {
+            int j = s_rowner[u >> 5];
+            while (j + 1 < n_round && s_span[j + 1].row0 <= (uint32_t)u) j++;
+            const SpanRec &S = s_span[j];
             const TriRec &R = s_rec[j];
-            uint32_t pix;
-            double z;
-            if (!eval_candidate(p, R, c - (int)R.cand0, s_vxy64, s_viz, pix, z)) continue;
-            const uint32_t F = s_dbits[pix];
-            if (__float_as_uint((float)z) != F) continue;
-            if (pass == 0) {
-              atomicMax(&s_wkey[pix],
-                        z < (double)__uint_as_float(F) ? 0x10000u + j : 0xFFFFu - j);
-            } else if (resolve_winner(s_wkey[pix], s_dec[pix]) == j) {
-              put_rgb(s_col, pix, R.rgb);
+            const int row = (int)S.py0 + (u - (int)S.row0);
+            int x0;
+            const int len = row_span(S, row, x0);
+            for (int px = x0; px < x0 + len; px++) {
+              double z;
+              if (!eval_exact(R, px, row, s_vxy64, s_viz, z)) continue;
+              const uint32_t pix = (uint32_t)(row * p.W + px);
+              const uint32_t F = s_dbits[pix];
+              if (__float_as_uint((float)z) != F) continue;
+              if (pass == 0) {
+                const uint32_t hb = s_wkey[pix] & kDecBit;
+                atomicMax(&s_wkey[pix],
+                          hb | (z < (double)__uint_as_float(F) ? 0x10000u + j : 0xFFFFu - j));
+              } else if (resolve_winner(s_wkey[pix]) == j) {
+                put_rgb(s_col, pix, R.rgb);
+              }
             }
           }
           __syncthreads();
         }
-        if (r1 < n_live) {
-          for (int i = tid; i < npx; i += kThreads) {
-            s_wkey[i] = 0u;
-            s_dec[i] = 0;
-          }
-        }
+        if (r1 < n_live)
+          for (int i = tid; i < npx; i += kThreads) s_wkey[i] = 0u;
       }
       __syncthreads();
       r0 = r1;
@@ -762,6 +853,7 @@ render_step_kernel(const RenderParams p) {
 
     // ---- phase 5: composite + postprocess (distractor.py:140-176, env.py:168-173)
     if (p.mode == PXR_MODE_VIDEO && p.vframe_bulk) mbar_wait_parity(&es.vbar, vphase);
+    vphase ^= 1u;
     const uint8_t *vsrc = p.mode == PXR_MODE_VIDEO
                               ? (p.vframe_bulk ? s_vframe
                                                : p.frames + es.frame_idx * p.vframe_bytes)
@@ -777,65 +869,94 @@ render_step_kernel(const RenderParams p) {
         bneg[byte >> 2] |= (uint32_t)(bc < 0 ? -bc : 0) << (8 * (byte & 3));
       }
     }
+    const bool row_groups = (p.W & 3) == 0;  // a 4-pixel group never wraps a row
     const int ngroups = npx >> 2;
-    for (int gi = tid; gi < ngroups + (npx & 3); gi += kThreads) {
-      const bool tail = gi >= ngroups;
-      const int i0 = tail ? (ngroups << 2) + (gi - ngroups) : (gi << 2);
-      const int np_ = tail ? 1 : 4;
-      float d[4];
+    for (int gi = tid; gi < ngroups; gi += kThreads) {
+      const int i0 = gi << 2;
+      const float4 d4 = reinterpret_cast<const float4 *>(s_depth)[gi];
+      const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+      const bool bg[4] = {isinf(d4.x), isinf(d4.y), isinf(d4.z), isinf(d4.w)};
+      uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
       uint32_t w[3];
-      if (!tail) {
-        const float4 d4 = reinterpret_cast<const float4 *>(s_depth)[gi];
-        d[0] = d4.x; d[1] = d4.y; d[2] = d4.z; d[3] = d4.w;
-        const uint32_t *c3 = reinterpret_cast<const uint32_t *>(s_col) + 3 * gi;
-        w[0] = c3[0]; w[1] = c3[1]; w[2] = c3[2];
+      const bool video = p.mode == PXR_MODE_VIDEO;
+      if (video && bg[0] && bg[1] && bg[2] && bg[3]) {
+        w[0] = w[1] = w[2] = 0u;  // fully replaced below
       } else {
-        d[0] = s_depth[i0];
-        w[0] = s_col[3 * i0] | (s_col[3 * i0 + 1] << 8) | (s_col[3 * i0 + 2] << 16);
-        w[1] = w[2] = 0u;
+        w[0] = c3[0]; w[1] = c3[1]; w[2] = c3[2];
       }
-      if (p.mode == PXR_MODE_VIDEO) {  // distractor.py:172-176
+      if (video && (bg[0] | bg[1] | bg[2] | bg[3])) {  // distractor.py:172-176
         int y = (int)__umulhi((uint32_t)i0, p.wmagic);
         int x = i0 - y * p.W;
-        for (int k = 0; k < np_; k++) {
-          if (isinf(d[k])) {
-            const uint8_t *src = vsrc + ((int)s_rowmap[y] * p.Wv + (int)s_colmap[x]) * 3;
-            for (int ch = 0; ch < 3; ch++) {
-              const int byte = 3 * k + ch;
-              const int wi = byte >> 2, sh = 8 * (byte & 3);
-              w[wi] = (w[wi] & ~(0xffu << sh)) | ((uint32_t)src[ch] << sh);
-            }
+        if (p.vframe_bulk && row_groups) {
+          const uint32_t rb = s_rowmap[y];
+          const uint4 cm = *reinterpret_cast<const uint4 *>(s_colmap + x);
+          const uint32_t cms[4] = {cm.x, cm.y, cm.z, cm.w};
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            if (!bg[k]) continue;
+            const uint32_t off = rb + cms[k];  // 24-bit texel from two aligned words
+            const uint32_t *wp = reinterpret_cast<const uint32_t *>(s_vframe + (off & ~3u));
+            put_texel(w, k, __funnelshift_r(wp[0], wp[1], 8 * (off & 3u)) & 0xffffffu);
           }
-          if (++x == p.W) { x = 0; y++; }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            if (bg[k]) {
+              const uint8_t *src = vsrc + s_rowmap[y] + s_colmap[x];
+              put_texel(w, k, (uint32_t)src[0] | ((uint32_t)src[1] << 8) |
+                                  ((uint32_t)src[2] << 16));
+            }
+            if (++x == p.W) { x = 0; y++; }
+          }
         }
       } else if (p.mode == PXR_MODE_COLOR) {  // distractor.py:149-161
         for (int q = 0; q < 3; q++) w[q] = __vsubus4(__vaddus4(w[q], bpos[q]), bneg[q]);
       }
       if (p.gray) {  // env.py:168-173
         uint32_t gw = 0;
-        for (int k = 0; k < np_; k++) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
           uint32_t ch3[3];
+#pragma unroll
           for (int ch = 0; ch < 3; ch++) {
             const int byte = 3 * k + ch;
             ch3[ch] = (w[byte >> 2] >> (8 * (byte & 3))) & 0xffu;
           }
           gw |= ((299u * ch3[0] + 587u * ch3[1] + 114u * ch3[2] + 500u) / 1000u) << (8 * k);
         }
-        if (!tail) reinterpret_cast<uint32_t *>(s_gray)[gi] = gw;
-        else s_gray[i0] = (uint8_t)gw;
-      } else if (!tail) {
-        uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
-        c3[0] = w[0]; c3[1] = w[1]; c3[2] = w[2];
+        reinterpret_cast<uint32_t *>(s_gray)[gi] = gw;
       } else {
-        put_rgb(s_col, (uint32_t)i0, w[0]);
+        c3[0] = w[0]; c3[1] = w[1]; c3[2] = w[2];
       }
       if (p.out_depth != nullptr) {
         float *dd = p.out_depth + (int64_t)env * npx + i0;
-        if (!tail && p.depth_vec) *reinterpret_cast<float4 *>(dd) = make_float4(d[0], d[1], d[2], d[3]);
-        else for (int k = 0; k < np_; k++) dd[k] = d[k];
+        if (p.depth_vec) *reinterpret_cast<float4 *>(dd) = d4;
+        else for (int k = 0; k < 4; k++) dd[k] = d[k];
       }
     }
-    vphase ^= 1u;
+    for (int i = (ngroups << 2) + tid; i < npx; i += kThreads) {  // tail pixels
+      const float d = s_depth[i];
+      uint32_t rgb = s_col[3 * i] | (s_col[3 * i + 1] << 8) | (s_col[3 * i + 2] << 16);
+      if (p.mode == PXR_MODE_VIDEO && isinf(d)) {
+        const int y = (int)__umulhi((uint32_t)i, p.wmagic), x = i - y * p.W;
+        const uint8_t *src = vsrc + s_rowmap[y] + s_colmap[x];
+        rgb = (uint32_t)src[0] | ((uint32_t)src[1] << 8) | ((uint32_t)src[2] << 16);
+      } else if (p.mode == PXR_MODE_COLOR) {
+        uint32_t o = 0;
+        for (int ch = 0; ch < 3; ch++) {
+          const int v = (int)((rgb >> (8 * ch)) & 0xffu) + es.bias[ch];
+          o |= (uint32_t)min(255, max(0, v)) << (8 * ch);
+        }
+        rgb = o;
+      }
+      if (p.gray) {
+        s_gray[i] = (uint8_t)((299u * (rgb & 0xffu) + 587u * ((rgb >> 8) & 0xffu) +
+                               114u * ((rgb >> 16) & 0xffu) + 500u) / 1000u);
+      } else {
+        put_rgb(s_col, (uint32_t)i, rgb);
+      }
+      if (p.out_depth != nullptr) p.out_depth[(int64_t)env * npx + i] = d;
+    }
 
     // ---- phase 6: frame -> HBM (one TMA bulk store) --------------------
     uint8_t *gout = p.out + (int64_t)env * p.frame_bytes;
@@ -1017,20 +1138,25 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   if (npx64 > (1 << 20) || height > 4096 || width > 4096)
     return set_unsupported("frame too large");
   p.wmagic = (uint32_t)((0x100000000ull + (uint64_t)width - 1) / (uint64_t)width);
+  p.gmagic = (uint32_t)((0x100000000ull + (uint64_t)(width / 4) - 1) / (uint64_t)(width / 4));
   p.depth_vec = out_depth != nullptr && (npx64 % 4 == 0) &&
                 ((reinterpret_cast<uintptr_t>(out_depth) & 15) == 0);
   p.frame_bytes = (int)(npx64 * C);
   p.use_bulk = (p.frame_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(out_obs) & 15) == 0);
   // Test hooks (tests/test_gpu_parity.py): shrink the per-round budgets so
   // the multi-round and fragment-overflow paths run on small inputs.
-  p.round_cand = kRoundCand;
   p.frag_limit = kFragCap;
+  p.row_cap = kRowCap > p.H ? kRowCap : p.H;
   int debug_cap = 0;
-  if (const char *s = getenv("PXR_DEBUG_ROUND_CAND")) p.round_cand = atoi(s) > 0 ? atoi(s) : kRoundCand;
-  if (const char *s = getenv("PXR_DEBUG_FRAG_LIMIT")) p.frag_limit = atoi(s) >= 0 ? min(atoi(s), kFragCap) : kFragCap;
+  if (const char *s = getenv("PXR_DEBUG_FRAG_LIMIT")) {
+    const int v = atoi(s);
+    if (v >= 0 && v < kFragCap) p.frag_limit = v;
+  }
+  if (const char *s = getenv("PXR_DEBUG_ROW_CAP")) {
+    const int v = atoi(s);
+    if (v > 0) p.row_cap = v > p.H ? v : p.H;
+  }
   if (const char *s = getenv("PXR_DEBUG_CAP")) debug_cap = atoi(s);
-  // one round's candidates never exceed max(round budget, one triangle's bbox)
-  p.chunk_cap = (int)((npx64 > p.round_cand ? npx64 : p.round_cand) / 32 + 2);
 
   int dev = 0;
   cudaGetDevice(&dev);

@@ -121,7 +121,7 @@ class TestRenderGolden:
 
     @pytest.mark.parametrize("knobs", [
         {"PXR_DEBUG_CAP": "40"},                       # many record rounds
-        {"PXR_DEBUG_ROUND_CAND": "300"},               # many candidate rounds
+        {"PXR_DEBUG_ROW_CAP": "90"},                   # many bbox-row rounds
         {"PXR_DEBUG_FRAG_LIMIT": "16"},                # fragment-list overflow path
         {"PXR_DEBUG_CAP": "24", "PXR_DEBUG_FRAG_LIMIT": "0"},
     ])
