@@ -78,14 +78,15 @@ struct __align__(16) TriRec {
 };
 static_assert(sizeof(TriRec) == 80, "TriRec layout");
 
-// ... and its conservative row-span data (see for_row_span).
+// ... and its conservative row-span data (see span_setup / row_span).
 struct __align__(16) SpanRec {
-  float r[3], c0[3], addu[3], addl[3];  // x-bounds: fma(r, y, c0) + add{u,l}
-  float hsy[3], hA[3];                  // horizontal edges: row sign test
-  uint16_t px0, px1, py0, pad;
-  uint32_t row0;                        // first row unit of the triangle
+  float r[3], c0[3], m[3];  // per edge: x-bound fma(r, y, c0) -/+ margin m,
+                            // or (horizontal edge) c0 = s.y
+  uint16_t px0, px1, py0;
+  uint16_t kinds;           // 2 bits per edge: 0 upper, 1 lower, 2 horiz A>0, 3 horiz A<0
+  uint32_t row0;            // first row unit of the triangle in the round
 };
-static_assert(sizeof(SpanRec) == 96, "SpanRec layout");
+static_assert(sizeof(SpanRec) == 48, "SpanRec layout");
 
 struct Frag {
   double z;      // f64 depth of the candidate (render.py:450-451)
@@ -303,27 +304,25 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 __device__ __forceinline__ void span_setup(const float2 a, const float2 b, const float2 c,
                                            float ymax, SpanRec &S) {
   const float2 v[3] = {a, b, c};
-  const float inf = __int_as_float(0x7f800000);
+  uint32_t kinds = 0;
 #pragma unroll
   for (int k = 0; k < 3; k++) {
     const float2 s = v[k], t = v[(k + 1) % 3];
     const float A = t.x - s.x, B = t.y - s.y;
-    S.hsy[k] = s.y;
-    S.hA[k] = B == 0.0f ? A : 0.0f;
     if (B != 0.0f) {
       const float r = A / B;
       S.r[k] = r;
       S.c0[k] = __fmaf_rn(-r, s.y, s.x);
-      const float m = 0x1p-10f + (fabsf(s.x) + fabsf(r) * (fabsf(s.y) + ymax)) * 0x1p-17f;
-      S.addu[k] = B > 0.0f ? m : inf;
-      S.addl[k] = B < 0.0f ? -m : -inf;
-    } else {
+      S.m[k] = 0x1p-10f + (fabsf(s.x) + fabsf(r) * (fabsf(s.y) + ymax)) * 0x1p-17f;
+      kinds |= (B > 0.0f ? 0u : 1u) << (2 * k);
+    } else {  // horizontal edge: only the sign of A * (y - s.y) matters
       S.r[k] = 0.0f;
-      S.c0[k] = 0.0f;
-      S.addu[k] = inf;
-      S.addl[k] = -inf;
+      S.c0[k] = s.y;
+      S.m[k] = 0.0f;
+      kinds |= (A > 0.0f ? 2u : 3u) << (2 * k);
     }
   }
+  S.kinds = (uint16_t)kinds;
 }
 
 // Conservative span of one bbox row: first pixel x0 and length (0 = empty).
@@ -331,13 +330,16 @@ __device__ __forceinline__ int row_span(const SpanRec &S, int py, int &x0) {
   const float y = (float)py + 0.5f;
   float lo = (float)S.px0 + 0.5f, hi = (float)S.px1 + 0.5f;
   bool empty = false;
+  const uint32_t kinds = S.kinds;
 #pragma unroll
   for (int k = 0; k < 3; k++) {
+    const uint32_t kind = (kinds >> (2 * k)) & 3u;
     const float x = __fmaf_rn(S.r[k], y, S.c0[k]);
-    hi = fminf(hi, __fadd_rn(x, S.addu[k]));  // NaN (inf - inf) is ignored
-    lo = fmaxf(lo, __fadd_rn(x, S.addl[k]));
-    const float dy = y - S.hsy[k];
-    empty |= (S.hA[k] > 0.0f && dy < 0.0f) || (S.hA[k] < 0.0f && dy > 0.0f);
+    const float ub = __fadd_rn(x, S.m[k]), lb = __fsub_rn(x, S.m[k]);
+    if (kind == 0u) hi = fminf(hi, ub);  // NaN bounds are ignored by fmin/fmax
+    if (kind == 1u) lo = fmaxf(lo, lb);
+    const float dy = y - S.c0[k];  // exact sign of pcy - s.y
+    empty |= (kind == 2u && dy < 0.0f) || (kind == 3u && dy > 0.0f);
   }
   const float xa = fmaxf(ceilf(lo - 0.5f), (float)S.px0);
   const float xb = fminf(floorf(hi - 0.5f), (float)S.px1);
@@ -710,7 +712,6 @@ render_step_kernel(const RenderParams p) {
         S.px0 = (uint16_t)(int)bx0;
         S.px1 = (uint16_t)(int)bx1;
         S.py0 = (uint16_t)(int)by0;
-        S.pad = 0;
         const uint32_t u0 = s_lrp[li] - rbase;
         S.row0 = u0;
         s_span[li - r0] = S;

@@ -1,5 +1,6 @@
-"""Profiling driver: set up one bench workload and run a few fused steps
-(no soak, no CPU legs) so ncu can capture the render kernel in isolation."""
+"""Profiling driver: set up one bench workload and run fused steps (no soak,
+no CPU legs) so ncu can capture the render kernel in isolation; prints the
+mean device time of the last --timed launches."""
 import argparse
 import os
 import sys
@@ -14,18 +15,20 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--model", default="Humanoid")
 ap.add_argument("--envs", type=int, default=4096)
 ap.add_argument("--mode", default="video")
-ap.add_argument("--steps", type=int, default=6)
+ap.add_argument("--steps", type=int, default=4)
+ap.add_argument("--timed", type=int, default=20)
 ap.add_argument("--grayscale", action="store_true")
 a = ap.parse_args()
 w = Workload(a.model, a.envs, a.mode, grayscale=a.grayscale)
 poses = [w.poses(t).clone() for t in range(2)]
 torch.cuda.synchronize()
-ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for t in range(a.steps):
-    if t == a.steps - 1:
-        ev[0].record()
     w.render(poses[t % 2], t)
-    if t == a.steps - 1:
-        ev[1].record()
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+ev[0].record()
+for t in range(a.timed):
+    w.render(poses[t % 2], a.steps + t)
+ev[1].record()
 torch.cuda.synchronize()
-print(f"{a.model} {a.mode} B={a.envs}: last launch {ev[0].elapsed_time(ev[1]):.3f} ms")
+ms = ev[0].elapsed_time(ev[1]) / max(1, a.timed)
+print(f"{a.model} {a.mode} B={a.envs}: {ms:.3f} ms/launch  {a.envs / ms / 1e3:.2f} M env-steps/s")
