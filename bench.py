@@ -148,16 +148,17 @@ def run_ours(args, world, rank, local):
     import torch
     import torch.distributed as tdist
 
-    from paper_2502_00021_b200 import _native
     from paper_2502_00021_b200.bench_support import Workload
+    from paper_2502_00021_b200.shards import aggregate, gather_stats, shard_envs
 
     if world > 1:
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     B = args.envs
-    w = Workload(args.model, B, args.mode, seed=0, env_offset=rank * B,
-                 logical_batch=world * B, grayscale=args.grayscale, device=dev)
+    shard = shard_envs(rank, world, B)  # envs [r*B, (r+1)*B) of world*B, no hot-path collective
+    w = Workload(args.model, B, args.mode, seed=0, env_offset=shard.env_offset,
+                 logical_batch=shard.logical_batch, grayscale=args.grayscale, device=dev)
     stream = torch.cuda.Stream(device=dev)
     n_pose_sets = 8
     obs_bytes = B * w.obs_bytes_per_env()
@@ -220,11 +221,10 @@ def run_ours(args, world, rank, local):
     if not args.no_e2e:
         e2e = run_e2e(args, w, dev, world, rank)
 
-    # ---- final stats gather (NCCL) -----------------------------------------
-    stats = torch.tensor([B * args.steps, ms, rank], dtype=torch.float64, device=dev)
+    # ---- final stats gather (NCCL): the only collective --------------------
+    stats = gather_stats({"env_steps": B * args.steps, "ms": ms, "mismatches": 0})
+    agg = aggregate(stats)
     if world > 1:
-        allst = [torch.empty_like(stats) for _ in range(world)]
-        tdist.all_gather(allst, stats)
         tdist.destroy_process_group()
 
     if rank != 0:
@@ -270,6 +270,8 @@ def run_ours(args, world, rank, local):
             "kernel": "render_step_kernel",
         },
         "gpu_launches": args.steps,
+        "stats_gather": {"ranks": len(stats), "env_steps": agg["env_steps"],
+                         "ms_max": agg["ms_max"]},
         "e2e": e2e,
         "clocks": clocks,
     }
