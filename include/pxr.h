@@ -183,6 +183,43 @@ pxr_status pxr_pose_source(const double *rest_qpos, const int32_t *parent,
                            uint64_t env_offset, int64_t t, int64_t batch,
                            double *poses, void *stream);
 
+/* ---- physics (the producer of the poses) ---------- */
+
+/* ModelSpec + ModelArrays flattened (models.py:46-103, physics.py:75-96);
+ * device arrays of n_links entries (joint arrays: n_links - 1). */
+typedef struct pxr_model {
+  const int32_t *parent;      /* (L) parent link, -1 for the root         */
+  const double *anchor_dist;  /* (L) joint anchor distance along parent   */
+  const double *length, *mass, *inertia;  /* (L)                          */
+  const double *limit_lo, *limit_hi, *torque_max;  /* (L - 1)             */
+  const double *rest_qpos;    /* (L + 2) reset centre                     */
+  int32_t n_links, substeps, fixed_root, has_min_root_height;
+  double dt, min_root_height, forward_weight, ctrl_cost;
+  int64_t episode_length;
+} pxr_model;
+
+/* One control step of step_dynamics (physics.py:427-465, _step_batch
+ * 272-420) for every env, in place, and reward += compute_reward
+ * (physics.py:468-477). done is set, never cleared. */
+pxr_status pxr_physics_step(const pxr_model *model, double *qpos, double *qvel,
+                            int64_t *step_count, uint8_t *done, const double *actions,
+                            double *reward, int64_t batch, void *stream);
+
+/* Reset draws (physics.py:487-510 / env.py:142-153, 226-238).
+ * mode 0: every env, key = split(key, .)[env_offset + i] (reset_state).
+ * mode 1: envs with done != 0 (auto-reset), key = fold_in(key_t, LB + g);
+ *         also the episode bookkeeping of env.py:219-238 (info_* outputs). */
+pxr_status pxr_reset_envs(const pxr_model *model, double *qpos, double *qvel,
+                          int64_t *step_count, uint8_t *done, double *ep_return,
+                          int64_t *ep_length, double *info_return, int64_t *info_length,
+                          const double *reward, int64_t batch, uint64_t key_hi,
+                          uint64_t key_lo, uint64_t env_offset, uint64_t logical_batch,
+                          int32_t mode, void *stream);
+
+/* forward_kinematics for an env's model: qpos (B, L + 2) -> poses (B, L, 3). */
+pxr_status pxr_env_poses(const pxr_model *model, const double *qpos, int64_t batch,
+                         double *poses, void *stream);
+
 /* forward_kinematics (physics.py:114-137): qpos (B, 3 + J) -> poses. */
 pxr_status pxr_forward_kinematics(const double *qpos, const int32_t *parent,
                                   const double *anchor_dist, int32_t n_links,

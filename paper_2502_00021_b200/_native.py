@@ -30,6 +30,7 @@ EXPORTED = (
     "pxr_render_step", "pxr_advance_distractors", "pxr_init_distractors",
     "pxr_apply_color", "pxr_apply_video", "pxr_grayscale", "pxr_threefry2x64",
     "pxr_sincosf", "pxr_pose_source", "pxr_forward_kinematics", "pxr_div_check",
+    "pxr_physics_step", "pxr_reset_envs", "pxr_env_poses",
 )
 
 _vp = ctypes.c_void_p
@@ -70,6 +71,17 @@ class VideoPackC(ctypes.Structure):
 class StepKeys(ctypes.Structure):
     _fields_ = [("key_hi", _u64), ("key_lo", _u64), ("env_offset", _u64),
                 ("logical_batch", _u64)]
+
+
+class Model(ctypes.Structure):
+    _fields_ = [
+        ("parent", _vp), ("anchor_dist", _vp), ("length", _vp), ("mass", _vp),
+        ("inertia", _vp), ("limit_lo", _vp), ("limit_hi", _vp), ("torque_max", _vp),
+        ("rest_qpos", _vp), ("n_links", _i32), ("substeps", _i32), ("fixed_root", _i32),
+        ("has_min_root_height", _i32), ("dt", ctypes.c_double),
+        ("min_root_height", ctypes.c_double), ("forward_weight", ctypes.c_double),
+        ("ctrl_cost", ctypes.c_double), ("episode_length", _i64),
+    ]
 
 
 _lib = None
@@ -131,6 +143,13 @@ def lib() -> ctypes.CDLL:
     L.pxr_pose_source.argtypes = [_vp, _vp, _vp, _i32, _u64, _u64, _u64, _i64, _i64, _vp, _vp]
     L.pxr_forward_kinematics.restype = _i32
     L.pxr_forward_kinematics.argtypes = [_vp, _vp, _vp, _i32, _i64, _vp, _vp]
+    L.pxr_physics_step.restype = _i32
+    L.pxr_physics_step.argtypes = [P(Model), _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]
+    L.pxr_reset_envs.restype = _i32
+    L.pxr_reset_envs.argtypes = [P(Model), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
+                                 _u64, _u64, _u64, _u64, _i32, _vp]
+    L.pxr_env_poses.restype = _i32
+    L.pxr_env_poses.argtypes = [P(Model), _vp, _i64, _vp, _vp]
     if L.pxr_abi_version() != 1:
         raise ImportError(f"{LIB_PATH}: ABI version {L.pxr_abi_version()} != 1")
     _lib = L

@@ -202,10 +202,46 @@ def replay_fixture(tag, model, batch, mode, steps, seed, observation="rgb",
     print(tag, "resets:", int(np.stack(dones).sum()), "final", h.hex()[:16])
 
 
+def physics_fixture():
+    """One control step of the reference's step_dynamics + compute_reward
+    (physics.py:427-477) from perturbed states, and reset_state draws
+    (physics.py:487-510), for every model."""
+    from pixelctrl.physics import SystemState, compute_reward, reset_state, step_dynamics
+
+    rec = {}
+    rng = np.random.default_rng(13)
+    for name in MODELS:
+        spec = spec_of(name)
+        B = 32
+        qpos = spec.rest()[None, :] + rng.uniform(-0.3, 0.3, (B, spec.dof))
+        qpos[:, 1] = rng.uniform(0.2, 1.5, B)  # some envs in ground contact
+        qvel = rng.normal(0.0, 0.5, (B, spec.dof))
+        act = rng.uniform(-1.3, 1.3, (B, spec.n_joints))  # includes clamped values
+        st = SystemState(qpos.copy(), qvel.copy(), rng.integers(0, 999, B).astype(np.int64),
+                         np.zeros(B, dtype=bool))
+        nxt = step_dynamics(spec, st, act)
+        rec[f"{name}_qpos"] = qpos
+        rec[f"{name}_qvel"] = qvel
+        rec[f"{name}_steps"] = st.step_count
+        rec[f"{name}_act"] = act
+        rec[f"{name}_qpos1"] = nxt.qpos
+        rec[f"{name}_qvel1"] = nxt.qvel
+        rec[f"{name}_done1"] = nxt.done
+        rec[f"{name}_reward"] = compute_reward(spec, st, nxt, act)
+        rs = reset_state(spec, fold_in(key_from_seed(3), 0x5EED), 16, env_offset=5)
+        rec[f"{name}_reset_qpos"] = rs.qpos
+        rec[f"{name}_reset_qvel"] = rs.qvel
+    np.savez_compressed(os.path.join(HERE, "physics.npz"), **rec)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "physics":
+        physics_fixture()
+        return
     geometry_fixture()
     render_fixtures()
     distractor_fixtures()
+    physics_fixture()
     pack = os.path.join("/tmp", "golden_replay.pxvp")
     small_pack(pack, seed=21, videos=4, frames=7, size=32)
     # BASELINE config 1: HalfCheetah, 1 env, 84x84, no distractors, 1000 steps.

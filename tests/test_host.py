@@ -130,3 +130,23 @@ class TestVideoPack:
         p.write_bytes(b"XXXX" + bytes(raw[4:]))
         with pytest.raises(PackFormatError, match="magic"):
             load_video_pack(p)
+
+
+class TestEnvConfig:  # reference tests/test_env.py:250-280
+    def test_round_trip_and_validation(self, tmp_path):
+        from paper_2502_00021_b200.env import EnvConfig, load_env_config, save_env_config
+
+        cfg = EnvConfig(model="walker_lite", batch=7, distractor_mode="color", seed=9,
+                        floor_in_background=True, logical_batch=20, env_offset=3)
+        p = tmp_path / "c.cfg"
+        save_env_config(cfg, p)
+        assert load_env_config(p) == cfg
+        assert load_env_config(p, batch=2).batch == 2
+        p.write_text("nope = 1\n")
+        with pytest.raises(ValueError, match="unknown config key"):
+            load_env_config(p)
+        with pytest.raises(ValueError, match="video_pack_path"):
+            EnvConfig(distractor_mode="video").validate()
+        with pytest.raises(ValueError, match="logical_batch"):
+            EnvConfig(batch=4, env_offset=2, logical_batch=5).validate()
+        assert EnvConfig(distractor_mode="video", video_pack_path="x").resolved_floor_in_background
