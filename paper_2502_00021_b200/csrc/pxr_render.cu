@@ -137,7 +137,7 @@ struct RenderParams {
 
 struct SmemLayout {
   int link, floor, maps, vxy64, viz, vxy32, vz, world, rows, ids, lrp, rec, span, rowner,
-      frag, depth, col, wkey, gray, vframe, total;
+      frag, depth, col, wkey, gray, gplan, vframe, total;
 };
 
 __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -165,7 +165,9 @@ __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   L.col = o;    o += align_up(npx * 3, 16);
   L.wkey = o;   o += align_up(npx * 4, 16);
   L.gray = o;   o += p.gray ? align_up(npx, 16) : 0;
-  L.vframe = o; o += p.mode == PXR_MODE_VIDEO ? align_up(p.vframe_bytes + 4, 16) : 0;
+  L.gplan = o;  o += p.mode == PXR_MODE_VIDEO ? align_up((p.W / 4 + 1) * 16, 16) : 0;
+  // + 32 B: the byte-permute gather may read up to 20 B past the last texel
+  L.vframe = o; o += p.mode == PXR_MODE_VIDEO ? align_up(p.vframe_bytes + 32, 16) : 0;
   L.total = o;
   return L;
 }
@@ -185,6 +187,7 @@ struct EnvShared {
   int n_rows;
   int chunk_next;
   int n_frag;
+  int plan_ok;
 };
 
 // Per-env distractor step (writes the new state back to HBM):
@@ -266,6 +269,29 @@ __device__ __forceinline__ void floor_px(const RenderParams &p, float ex, float 
       const uint32_t c = parity == 0 ? 158u : 122u;  // render.py:51-52
       rgb = c | (c << 8) | (c << 16);
       depth = (float)t;
+    }
+  }
+}
+
+// Clamped pixel range of a bbox side (render.py:390-403):
+// int(ceil(mn - 0.5)) .. int(floor(mx - 0.5)), lower end clamped to 0 and
+// upper end to lim (so lo > hi means empty). f64 in the reference; for
+// |v| < 2^21 the f32 value v - 0.5 is exact, so f32 ceil/floor give the same
+// integers without f64 conversions.
+__device__ __forceinline__ void pixel_range(float mn, float mx, int lim, int &lo, int &hi) {
+  if (fabsf(mn) < 0x1p21f && fabsf(mx) < 0x1p21f) {
+    lo = (int)fmaxf(ceilf(mn - 0.5f), 0.0f);
+    hi = (int)fminf(floorf(mx - 0.5f), (float)lim);
+  } else {
+    double a = ceil((double)mn - 0.5), b = floor((double)mx - 0.5);
+    if (a < 0.0) a = 0.0;
+    if (b > (double)lim) b = (double)lim;
+    if (a > b) {  // empty; keep the integers in range
+      lo = 1;
+      hi = 0;
+    } else {
+      lo = (int)a;
+      hi = (int)b;
     }
   }
 }
@@ -428,6 +454,7 @@ render_step_kernel(const RenderParams p) {
   uint32_t *s_wkey = reinterpret_cast<uint32_t *>(smem + L.wkey);
   uint8_t *s_gray = smem + L.gray;
   uint8_t *s_vframe = smem + L.vframe;
+  uint4 *s_gplan = reinterpret_cast<uint4 *>(smem + L.gplan);
   uint8_t *s_out = p.gray ? s_gray : s_col;
 
   const int tid = threadIdx.x;
@@ -461,8 +488,48 @@ render_step_kernel(const RenderParams p) {
   if (tid == 0) {
     mbar_init(&es.vbar, 1);
     fence_mbar_init();
+    es.plan_ok = 0;
   }
   __syncthreads();
+  // Byte-permute plan of the NN video gather (distractor.py:172-176): with
+  // W % 4 == 0 and 4-byte-aligned source rows, the 12 output bytes of a
+  // 4-pixel group come from one 24-byte window of the source row, and each
+  // output word from two consecutive source words -> 2 loads + one PRMT.
+  const bool use_plan = p.mode == PXR_MODE_VIDEO && p.vframe_bulk && (p.W & 3) == 0 &&
+                        ((p.Wv * 3) & 3) == 0;
+  if (use_plan) {
+    int bad = 0;
+    for (int gc = tid; gc < (p.W >> 2); gc += kThreads) {
+      const int x0 = gc * 4;
+      const uint32_t base_word = s_colmap[x0] >> 2;
+      uint4 pl;
+      pl.x = base_word;
+      uint32_t sel[3];
+      for (int q = 0; q < 3; q++) {
+        int r[4], rmin = 1 << 30;
+        for (int bb = 0; bb < 4; bb++) {
+          const int b = 4 * q + bb, k = b / 3, ch = b % 3;
+          r[bb] = (int)(s_colmap[x0 + k] + ch) - (int)(base_word * 4);
+          rmin = min(rmin, r[bb]);
+        }
+        const int a = rmin >> 2;
+        uint32_t s = (uint32_t)a << 16;
+        for (int bb = 0; bb < 4; bb++) {
+          const int nib = r[bb] - 4 * a;
+          if (nib < 0 || nib > 7 || a > 3) bad = 1;
+          s |= (uint32_t)(nib & 7) << (4 * bb);
+        }
+        sel[q] = s;
+      }
+      pl.y = sel[0];
+      pl.z = sel[1];
+      pl.w = sel[2];
+      s_gplan[gc] = pl;
+    }
+    if (bad) es.plan_ok = -1;
+  }
+  __syncthreads();
+  const bool plan_ok = use_plan && es.plan_ok == 0;
 
   uint32_t vphase = 0;
   int local_env = 0;
@@ -538,12 +605,9 @@ render_step_kernel(const RenderParams p) {
         if (area2 != 0.0f) {
           const float minx = fminf(a.x, fminf(b.x, c.x)), maxx = fmaxf(a.x, fmaxf(b.x, c.x));
           const float miny = fminf(a.y, fminf(b.y, c.y)), maxy = fmaxf(a.y, fmaxf(b.y, c.y));
-          double bx0 = ceil((double)minx - 0.5), bx1 = floor((double)maxx - 0.5);
-          double by0 = ceil((double)miny - 0.5), by1 = floor((double)maxy - 0.5);
-          if (bx0 < 0.0) bx0 = 0.0;
-          if (by0 < 0.0) by0 = 0.0;
-          if (bx1 > (double)(p.W - 1)) bx1 = (double)(p.W - 1);
-          if (by1 > (double)(p.H - 1)) by1 = (double)(p.H - 1);
+          int bx0, bx1, by0, by1;
+          pixel_range(minx, maxx, p.W - 1, bx0, bx1);
+          pixel_range(miny, maxy, p.H - 1, by0, by1);
           if (!(bx0 > bx1 || by0 > by1)) {
             const float *w0 = s_world + 3 * i0, *w1 = s_world + 3 * i1, *w2 = s_world + 3 * i2;
             const float e1x = w1[0] - w0[0], e1y = w1[1] - w0[1], e1z = w1[2] - w0[2];
@@ -552,7 +616,7 @@ render_step_kernel(const RenderParams p) {
             const float ny = e1z * e2x - e1x * e2z;
             const float nz = e1x * e2y - e1y * e2x;
             if (!((double)sqrtf(nx * nx + ny * ny + nz * nz) < 1e-20))
-              rows = (uint32_t)((int)(by1 - by0) + 1);
+              rows = (uint32_t)(by1 - by0 + 1);
           }
         }
       }
@@ -683,12 +747,9 @@ render_step_kernel(const RenderParams p) {
         }
         const float minx = fminf(a.x, fminf(b.x, c.x)), maxx = fmaxf(a.x, fmaxf(b.x, c.x));
         const float miny = fminf(a.y, fminf(b.y, c.y)), maxy = fmaxf(a.y, fmaxf(b.y, c.y));
-        double bx0 = ceil((double)minx - 0.5), bx1 = floor((double)maxx - 0.5);
-        double by0 = ceil((double)miny - 0.5), by1 = floor((double)maxy - 0.5);
-        if (bx0 < 0.0) bx0 = 0.0;
-        if (by0 < 0.0) by0 = 0.0;
-        if (bx1 > (double)(p.W - 1)) bx1 = (double)(p.W - 1);
-        if (by1 > (double)(p.H - 1)) by1 = (double)(p.H - 1);
+        int bx0, bx1, by0, by1;
+        pixel_range(minx, maxx, p.W - 1, bx0, bx1);
+        pixel_range(miny, maxy, p.H - 1, by0, by1);
         const float ax0 = b.x - a.x, ay0 = b.y - a.y;
         const float ax1 = c.x - b.x, ay1 = c.y - b.y;
         const float ax2 = a.x - c.x, ay2 = a.y - c.y;
@@ -709,13 +770,13 @@ render_step_kernel(const RenderParams p) {
         s_rec[li - r0] = R;
         SpanRec S;
         span_setup(a, b, c, (float)(p.H + 1), S);
-        S.px0 = (uint16_t)(int)bx0;
-        S.px1 = (uint16_t)(int)bx1;
-        S.py0 = (uint16_t)(int)by0;
+        S.px0 = (uint16_t)bx0;
+        S.px1 = (uint16_t)bx1;
+        S.py0 = (uint16_t)by0;
         const uint32_t u0 = s_lrp[li] - rbase;
         S.row0 = u0;
         s_span[li - r0] = S;
-        const uint32_t u1 = u0 + (uint32_t)((int)(by1 - by0) + 1);
+        const uint32_t u1 = u0 + (uint32_t)(by1 - by0 + 1);
         for (uint32_t k = (u0 + 31) >> 5; k <= ((u1 - 1) >> 5); k++)
           s_rowner[k] = (uint16_t)(li - r0);
       }
@@ -888,7 +949,22 @@ render_step_kernel(const RenderParams p) {
       if (video && (bg[0] | bg[1] | bg[2] | bg[3])) {  // distractor.py:172-176
         int y = (int)__umulhi((uint32_t)i0, p.wmagic);
         int x = i0 - y * p.W;
-        if (p.vframe_bulk && row_groups) {
+        if (plan_ok) {
+          const uint4 pl = s_gplan[x >> 2];
+          const uint32_t *src =
+              reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y]) + pl.x;
+          const uint32_t sels[3] = {pl.y, pl.z, pl.w};
+          const uint32_t m[3] = {
+              (bg[0] ? 0x00ffffffu : 0u) | (bg[1] ? 0xff000000u : 0u),
+              (bg[1] ? 0x0000ffffu : 0u) | (bg[2] ? 0xffff0000u : 0u),
+              (bg[2] ? 0x000000ffu : 0u) | (bg[3] ? 0xffffff00u : 0u)};
+#pragma unroll
+          for (int q = 0; q < 3; q++) {
+            const uint32_t *wp = src + (sels[q] >> 16);
+            const uint32_t t = __byte_perm(wp[0], wp[1], sels[q] & 0xffffu);
+            w[q] = (t & m[q]) | (w[q] & ~m[q]);
+          }
+        } else if (p.vframe_bulk && row_groups) {
           const uint32_t rb = s_rowmap[y];
           const uint4 cm = *reinterpret_cast<const uint4 *>(s_colmap + x);
           const uint32_t cms[4] = {cm.x, cm.y, cm.z, cm.w};
