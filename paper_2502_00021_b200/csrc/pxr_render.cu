@@ -941,30 +941,27 @@ render_step_kernel(const RenderParams p) {
       uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
       uint32_t w[3];
       const bool video = p.mode == PXR_MODE_VIDEO;
-      if (video && bg[0] && bg[1] && bg[2] && bg[3]) {
-        w[0] = w[1] = w[2] = 0u;  // fully replaced below
-      } else {
-        w[0] = c3[0]; w[1] = c3[1]; w[2] = c3[2];
-      }
-      if (video && (bg[0] | bg[1] | bg[2] | bg[3])) {  // distractor.py:172-176
+      w[0] = c3[0]; w[1] = c3[1]; w[2] = c3[2];
+      if (plan_ok) {  // branch-free: texel words merged under per-pixel byte masks
+        const int y = (int)__umulhi((uint32_t)i0, p.wmagic);
+        const int x = i0 - y * p.W;
+        const uint4 pl = s_gplan[x >> 2];
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y]) + pl.x;
+        const uint32_t sels[3] = {pl.y, pl.z, pl.w};
+        const uint32_t m[3] = {
+            (bg[0] ? 0x00ffffffu : 0u) | (bg[1] ? 0xff000000u : 0u),
+            (bg[1] ? 0x0000ffffu : 0u) | (bg[2] ? 0xffff0000u : 0u),
+            (bg[2] ? 0x000000ffu : 0u) | (bg[3] ? 0xffffff00u : 0u)};
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+          const uint32_t *wp = src + (sels[q] >> 16);
+          const uint32_t t = __byte_perm(wp[0], wp[1], sels[q] & 0xffffu);
+          w[q] = (t & m[q]) | (w[q] & ~m[q]);
+        }
+      } else if (video && (bg[0] | bg[1] | bg[2] | bg[3])) {  // distractor.py:172-176
         int y = (int)__umulhi((uint32_t)i0, p.wmagic);
         int x = i0 - y * p.W;
-        if (plan_ok) {
-          const uint4 pl = s_gplan[x >> 2];
-          const uint32_t *src =
-              reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y]) + pl.x;
-          const uint32_t sels[3] = {pl.y, pl.z, pl.w};
-          const uint32_t m[3] = {
-              (bg[0] ? 0x00ffffffu : 0u) | (bg[1] ? 0xff000000u : 0u),
-              (bg[1] ? 0x0000ffffu : 0u) | (bg[2] ? 0xffff0000u : 0u),
-              (bg[2] ? 0x000000ffu : 0u) | (bg[3] ? 0xffffff00u : 0u)};
-#pragma unroll
-          for (int q = 0; q < 3; q++) {
-            const uint32_t *wp = src + (sels[q] >> 16);
-            const uint32_t t = __byte_perm(wp[0], wp[1], sels[q] & 0xffffu);
-            w[q] = (t & m[q]) | (w[q] & ~m[q]);
-          }
-        } else if (p.vframe_bulk && row_groups) {
+        if (p.vframe_bulk && row_groups) {
           const uint32_t rb = s_rowmap[y];
           const uint4 cm = *reinterpret_cast<const uint4 *>(s_colmap + x);
           const uint32_t cms[4] = {cm.x, cm.y, cm.z, cm.w};
