@@ -698,8 +698,13 @@ render_step_kernel(const RenderParams p) {
     for (int r0 = 0; r0 < n_live;) {
       if (tid == 0) {
         // live [r0, r1): at most cap triangles and row_cap bbox rows (a
-        // single triangle always fits: row_cap >= H)
-        int lo = r0 + 1, hi = min(r0 + p.cap, n_live);
+        // single triangle always fits: row_cap >= H); when several rounds
+        // are needed their triangle counts are balanced (a small last round
+        // cannot fill the CTA)
+        const int left = n_live - r0;
+        const int n_rounds = (left + p.cap - 1) / p.cap;
+        const int target = (left + n_rounds - 1) / n_rounds;
+        int lo = r0 + 1, hi = min(r0 + target, n_live);
         const uint32_t base = s_lrp[r0];
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
