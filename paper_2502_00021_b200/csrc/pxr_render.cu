@@ -146,7 +146,7 @@ __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   SmemLayout L;
   int o = 0;
   const int npx = p.H * p.W;
-  L.link = o;   o += align_up(p.nl * 16, 16);
+  L.link = o;   o += align_up(2 * p.nl * 16, 16);  // double-buffered (prefetch)
   L.floor = o;  o += align_up((p.W + 2 * p.H) * 8, 16);
   L.maps = o;   o += align_up((p.W + p.H) * 4, 16);  // texel byte offsets per row / column
   L.vxy64 = o;  o += align_up(p.nv * 16, 16);
@@ -179,9 +179,9 @@ struct DistSlot {
 
 struct EnvShared {
   uint64_t vbar;  // mbarrier for the video frame bulk load
-  float ex, ez;
-  int bias[3];
-  int64_t frame_idx;
+  int64_t frame_idx[2];  // [local_env & 1]: prepared one env ahead
+  float ex[2], ez[2];
+  int bias[2][3];
   int n_live;
   int round_end;
   int n_rows;
@@ -297,6 +297,40 @@ __device__ __forceinline__ void pixel_range(float mn, float mx, int lim, int &lo
 }
 
 // World-space vertex v (render.py:470-481): f32, no FMA contraction.
+// Per-env inputs of the first phases, prepared by one warp one env ahead so
+// the glibc-exact sincosf chains (render.py:613-614) and the Threefry chains
+// overlap the previous env's rasterisation instead of stalling the CTA:
+// link (x, z, cos, sin) into link_buf; camera position and the distractor
+// bias / frame index into es[local_env & 1]. The distractor state of 32
+// envs of this CTA is advanced at once, one lane each.
+__device__ __forceinline__ void prepare_env(const RenderParams &p, int64_t env, int local_env,
+                                         float4 *link_buf, DistSlot *s_dist, EnvShared &es,
+                                         int lane) {
+  for (int l = lane; l < p.nl; l += 32) {
+    const double *pp = p.poses + (env * p.nl + l) * 3;
+    const float th = (float)pp[2];  // poses.astype(float32), render.py:613
+    link_buf[l] = make_float4((float)pp[0], (float)pp[1], glibc_sincosf(th, 1),
+                              glibc_sincosf(th, 0));
+  }
+  if (local_env % 32 == 0) {
+    const int64_t e2 = env + (int64_t)lane * gridDim.x;
+    if (e2 < p.batch) distractor_update(p, e2, s_dist[lane]);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const int b = local_env & 1;
+    const double *p0 = p.poses + env * p.nl * 3;
+    es.ex[b] = (float)(p0[0] + p.off_x);  // render.py:611
+    es.ez[b] = (float)(p0[1] + p.off_z);  // render.py:612
+    const DistSlot &ds = s_dist[local_env % 32];
+    es.bias[b][0] = ds.bias[0];
+    es.bias[b][1] = ds.bias[1];
+    es.bias[b][2] = ds.bias[2];
+    es.frame_idx[b] = ds.frame_idx;
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ float3 world_vertex(const RenderParams &p, const float4 *s_link, int v) {
   const float4 lk = s_link[__ldg(p.vert_link + v)];
   const float bx = __ldg(p.base_verts + 3 * v + 0);
@@ -531,46 +565,28 @@ render_step_kernel(const RenderParams p) {
   __syncthreads();
   const bool plan_ok = use_plan && es.plan_ok == 0;
 
+  if (warp == kWarps - 1 && blockIdx.x < p.batch)
+    prepare_env(p, blockIdx.x, 0, s_link, s_dist, es, lane);
+  __syncthreads();
+
   uint32_t vphase = 0;
   int local_env = 0;
   for (int64_t env = blockIdx.x; env < p.batch; env += gridDim.x, local_env++) {
-    // ---- phase 0: per-link trig, camera, distractor state, video fetch ---
-    for (int l = tid; l < p.nl; l += kThreads) {
-      const double *pp = p.poses + ((int64_t)env * p.nl + l) * 3;
-      const float th = (float)pp[2];  // poses.astype(float32), render.py:613
-      s_link[l] = make_float4((float)pp[0], (float)pp[1], glibc_sincosf(th, 1),
-                              glibc_sincosf(th, 0));
+    // ---- phase 0: video fetch (the env's link trig, camera and distractor
+    // state were prepared by warp kWarps-1 during the previous env) -------
+    const int cb = local_env & 1;
+    const float4 *s_link_cur = s_link + cb * p.nl;
+    if (tid == 0 && p.mode == PXR_MODE_VIDEO && p.vframe_bulk) {
+      mbar_arrive_expect_tx(&es.vbar, (uint32_t)p.vframe_bytes);
+      bulk_load_g2s(s_vframe, p.frames + es.frame_idx[cb] * p.vframe_bytes,
+                    (uint32_t)p.vframe_bytes, &es.vbar);
     }
-    if (warp == kWarps - 1) {
-      // Distractor state of the next 32 envs of this CTA, one lane each, in
-      // lockstep (the Threefry chains then cost one env's latency per 32).
-      if (local_env % 32 == 0) {
-        const int64_t e2 = env + (int64_t)lane * gridDim.x;
-        if (e2 < p.batch) distractor_update(p, e2, s_dist[lane]);
-        __syncwarp();
-      }
-      if (lane == 0) {
-        const double *p0 = p.poses + (int64_t)env * p.nl * 3;
-        es.ex = (float)(p0[0] + p.off_x);  // render.py:611
-        es.ez = (float)(p0[1] + p.off_z);  // render.py:612
-        const DistSlot &ds = s_dist[local_env % 32];
-        es.bias[0] = ds.bias[0];
-        es.bias[1] = ds.bias[1];
-        es.bias[2] = ds.bias[2];
-        es.frame_idx = ds.frame_idx;
-        if (p.mode == PXR_MODE_VIDEO && p.vframe_bulk) {
-          mbar_arrive_expect_tx(&es.vbar, (uint32_t)p.vframe_bytes);
-          bulk_load_g2s(s_vframe, p.frames + ds.frame_idx * p.vframe_bytes,
-                        (uint32_t)p.vframe_bytes, &es.vbar);
-        }
-      }
-    }
-    __syncthreads();
-    const float ex = es.ex, ez = es.ez;
+    const float ex = es.ex[cb], ez = es.ez[cb];
+    bool prepared = env + gridDim.x >= p.batch;  // nothing to prepare for a last env
 
     // ---- phase 1: world transform + projection (render.py:468-481, 350-363)
     for (int v = tid; v < p.nv; v += kThreads) {
-      const float3 w = world_vertex(p, s_link, v);
+      const float3 w = world_vertex(p, s_link_cur, v);
       s_world[3 * v + 0] = w.x;
       s_world[3 * v + 1] = w.y;
       s_world[3 * v + 2] = w.z;
@@ -791,6 +807,11 @@ render_step_kernel(const RenderParams p) {
       // dynamically; each lane computes one row span, the warp expands the
       // chunk's spans into candidates and runs the exact test on them.
       const int n_chunks = (n_rows + 31) >> 5;
+      if (warp == kWarps - 1 && !prepared) {  // joins the chunk queue afterwards
+        prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
+                    lane);
+        prepared = true;
+      }
       while (true) {
         int k = 0;
         if (lane == 0) k = atomicAdd(&es.chunk_next, 1);
@@ -917,13 +938,15 @@ render_step_kernel(const RenderParams p) {
       __syncthreads();
       r0 = r1;
     }
+    if (warp == kWarps - 1 && !prepared)  // env without live triangles
+      prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es, lane);
 
     // ---- phase 5: composite + postprocess (distractor.py:140-176, env.py:168-173)
     if (p.mode == PXR_MODE_VIDEO && p.vframe_bulk) mbar_wait_parity(&es.vbar, vphase);
     vphase ^= 1u;
     const uint8_t *vsrc = p.mode == PXR_MODE_VIDEO
                               ? (p.vframe_bulk ? s_vframe
-                                               : p.frames + es.frame_idx * p.vframe_bytes)
+                                               : p.frames + es.frame_idx[cb] * p.vframe_bytes)
                               : nullptr;
     // Four consecutive pixels per thread: 12 colour bytes are three aligned
     // words; the colour bias is a per-byte saturating add/sub (__vaddus4 /
@@ -931,7 +954,7 @@ render_step_kernel(const RenderParams p) {
     uint32_t bpos[3] = {0u, 0u, 0u}, bneg[3] = {0u, 0u, 0u};
     if (p.mode == PXR_MODE_COLOR) {
       for (int byte = 0; byte < 12; byte++) {
-        const int bc = es.bias[byte % 3];
+        const int bc = es.bias[cb][byte % 3];
         bpos[byte >> 2] |= (uint32_t)(bc > 0 ? bc : 0) << (8 * (byte & 3));
         bneg[byte >> 2] |= (uint32_t)(bc < 0 ? -bc : 0) << (8 * (byte & 3));
       }
@@ -1023,7 +1046,7 @@ render_step_kernel(const RenderParams p) {
       } else if (p.mode == PXR_MODE_COLOR) {
         uint32_t o = 0;
         for (int ch = 0; ch < 3; ch++) {
-          const int v = (int)((rgb >> (8 * ch)) & 0xffu) + es.bias[ch];
+          const int v = (int)((rgb >> (8 * ch)) & 0xffu) + es.bias[cb][ch];
           o |= (uint32_t)min(255, max(0, v)) << (8 * ch);
         }
         rgb = o;
