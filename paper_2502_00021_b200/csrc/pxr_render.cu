@@ -60,7 +60,7 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLinks = 64;
 constexpr uint32_t kFull = 0xffffffffu;
-constexpr int kRowCap = 4096;   // bbox rows per raster round (raised to H)
+constexpr int kRowCap = 2560;   // bbox rows (>= spans) per raster round (raised to H)
 constexpr int kFragCap = 1536;  // fragment list capacity (overflow: recompute)
 constexpr uint32_t kDecBit = 0x80000000u;
 
@@ -68,15 +68,16 @@ constexpr uint32_t kSkyRGB = 135u | (206u << 8) | (235u << 16);  // render.py:50
 
 // One live triangle of the current round (post-swap order, render.py:381-385):
 // the exact-test data ...
+// The f32 edge vectors and area are kept as f32: the reference converts them
+// to f64 exactly (render.py:437-449), so (double) on use is the same value.
 struct __align__(16) TriRec {
-  double A0, B0, A1, B1, A2, B2;  // (double) of the f32 edge vectors ax_k, ay_k
-  double rcp;                     // RN(1 / (double)area2), for the exact division
-  double area;                    // (double)area2
-  uint16_t v0, v1, v2, flags;     // vertex ids; top-left bits (render.py:431-433)
-  uint32_t rgb;                   // flat-shaded u8 colour (render.py:404-423)
-  uint32_t pad;
+  float A0, B0, A1, B1, A2, B2;  // f32 edge vectors ax_k, ay_k
+  float area;                    // area2
+  uint32_t rgb;                  // flat-shaded u8 colour (render.py:404-423)
+  double rcp;                    // RN(1 / (double)area2), for the exact division
+  uint16_t v0, v1, v2, flags;    // vertex ids; top-left bits (render.py:431-433)
 };
-static_assert(sizeof(TriRec) == 80, "TriRec layout");
+static_assert(sizeof(TriRec) == 48, "TriRec layout");
 
 // ... and its conservative row-span data (see span_setup / row_span).
 struct __align__(16) SpanRec {
@@ -87,6 +88,9 @@ struct __align__(16) SpanRec {
   uint32_t row0;            // first row unit of the triangle in the round
 };
 static_assert(sizeof(SpanRec) == 48, "SpanRec layout");
+// Non-empty spans wait in a per-warp queue as uint2 {x0 | len << 16,
+// row | live_tri << 16} until 32 can be evaluated together.
+constexpr int kQueue = 64;
 
 struct Frag {
   double z;      // f64 depth of the candidate (render.py:450-451)
@@ -136,7 +140,7 @@ struct RenderParams {
 };
 
 struct SmemLayout {
-  int link, floor, maps, vxy64, viz, vxy32, vz, world, rows, ids, lrp, rec, span, rowner,
+  int link, floor, maps, vxy64, viz, vxy32, vz, world, rows, ids, lrp, rec, span, rowner, queue,
       frag, depth, col, wkey, gray, gplan, vframe, total;
 };
 
@@ -160,6 +164,7 @@ __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   L.rec = o;    o += p.cap * (int)sizeof(TriRec);
   L.span = o;   o += align_up(p.cap * (int)sizeof(SpanRec), 16);
   L.rowner = o; o += align_up((p.row_cap / 32 + 2) * 2, 16);
+  L.queue = o;  o += kWarps * kQueue * 8;
   L.frag = o;   o += kFragCap * (int)sizeof(Frag);
   L.depth = o;  o += align_up(npx * 4, 16);
   L.col = o;    o += align_up(npx * 3, 16);
@@ -184,7 +189,6 @@ struct EnvShared {
   int bias[2][3];
   int n_live;
   int round_end;
-  int n_rows;
   int chunk_next;
   int n_frag;
   int plan_ok;
@@ -414,15 +418,16 @@ __device__ __forceinline__ bool eval_exact(const TriRec &R, int px, int py,
                                            double &z) {
   const double2 p0 = s_vxy64[R.v0], p1 = s_vxy64[R.v1], p2 = s_vxy64[R.v2];
   const double pcx = half_plus(px), pcy = half_plus(py);
-  const double e0 = R.A0 * (pcy - p0.y) - R.B0 * (pcx - p0.x);
-  const double e1 = R.A1 * (pcy - p1.y) - R.B1 * (pcx - p1.x);
-  const double e2 = R.A2 * (pcy - p2.y) - R.B2 * (pcx - p2.x);
+  const double e0 = (double)R.A0 * (pcy - p0.y) - (double)R.B0 * (pcx - p0.x);
+  const double e1 = (double)R.A1 * (pcy - p1.y) - (double)R.B1 * (pcx - p1.x);
+  const double e2 = (double)R.A2 * (pcy - p2.y) - (double)R.B2 * (pcx - p2.x);
   const uint32_t fl = R.flags;
   if ((e0 > 0.0 || (e0 == 0.0 && (fl & 1u))) && (e1 > 0.0 || (e1 == 0.0 && (fl & 2u))) &&
       (e2 > 0.0 || (e2 == 0.0 && (fl & 4u)))) {
-    const double l0 = div_rn_pre(e1, R.area, R.rcp);
-    const double l1 = div_rn_pre(e2, R.area, R.rcp);
-    const double l2 = div_rn_pre(e0, R.area, R.rcp);
+    const double area = (double)R.area;
+    const double l0 = div_rn_pre(e1, area, R.rcp);
+    const double l1 = div_rn_pre(e2, area, R.rcp);
+    const double l2 = div_rn_pre(e0, area, R.rcp);
     const double inv_z = l0 * s_viz[R.v0] + l1 * s_viz[R.v1] + l2 * s_viz[R.v2];
     z = __drcp_rn(inv_z);
     return true;
@@ -481,6 +486,7 @@ render_step_kernel(const RenderParams p) {
   TriRec *s_rec = reinterpret_cast<TriRec *>(smem + L.rec);
   SpanRec *s_span = reinterpret_cast<SpanRec *>(smem + L.span);
   uint16_t *s_rowner = reinterpret_cast<uint16_t *>(smem + L.rowner);
+  uint2 *s_queue = reinterpret_cast<uint2 *>(smem + L.queue);
   Frag *s_frag = reinterpret_cast<Frag *>(smem + L.frag);
   float *s_depth = reinterpret_cast<float *>(smem + L.depth);
   uint32_t *s_dbits = reinterpret_cast<uint32_t *>(smem + L.depth);
@@ -727,16 +733,15 @@ render_step_kernel(const RenderParams p) {
           if (s_lrp[mid] - base <= (uint32_t)p.row_cap) lo = mid; else hi = mid - 1;
         }
         es.round_end = lo;
-        es.n_rows = (int)(s_lrp[lo] - base);
         es.chunk_next = 0;
         es.n_frag = 0;
       }
       __syncthreads();
       const int r1 = es.round_end;
-      const int n_rows = es.n_rows;
-      const int n_round = r1 - r0;
       const uint32_t rbase = s_lrp[r0];
-      // records (render.py:366-436), span setup, row-chunk owners
+      const int n_rows = (int)(s_lrp[r1] - rbase);
+      const int n_round = r1 - r0;
+      // records (render.py:366-436), span line equations, row-chunk owners
       for (int li = r0 + tid; li < r1; li += kThreads) {
         const int t = s_ids[li];
         int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
@@ -779,15 +784,14 @@ render_step_kernel(const RenderParams p) {
         if (ay1 < 0.0f || (ay1 == 0.0f && ax1 > 0.0f)) fl |= 2u;
         if (ay2 < 0.0f || (ay2 == 0.0f && ax2 > 0.0f)) fl |= 4u;
         TriRec R;
-        R.A0 = (double)ax0; R.B0 = (double)ay0;
-        R.A1 = (double)ax1; R.B1 = (double)ay1;
-        R.A2 = (double)ax2; R.B2 = (double)ay2;
-        R.area = (double)area2;
-        R.rcp = __drcp_rn(R.area);
+        R.A0 = ax0; R.B0 = ay0;
+        R.A1 = ax1; R.B1 = ay1;
+        R.A2 = ax2; R.B2 = ay2;
+        R.area = area2;
+        R.rgb = rgb;
+        R.rcp = __drcp_rn((double)area2);
         R.v0 = (uint16_t)i0; R.v1 = (uint16_t)i1; R.v2 = (uint16_t)i2;
         R.flags = (uint16_t)fl;
-        R.rgb = rgb;
-        R.pad = 0;
         s_rec[li - r0] = R;
         SpanRec S;
         span_setup(a, b, c, (float)(p.H + 1), S);
@@ -804,78 +808,105 @@ render_step_kernel(const RenderParams p) {
       __syncthreads();
 
       // (triangle, bbox row) units, 32 per chunk, chunks scheduled
-      // dynamically; each lane computes one row span, the warp expands the
-      // chunk's spans into candidates and runs the exact test on them.
+      // dynamically: each lane computes one row's conservative span and the
+      // non-empty spans go to the warp's queue; whenever 32 are queued (and
+      // at the end) the warp expands 32 spans into pixel candidates and runs
+      // the exact test on them, so the f64 work runs on full warps even
+      // though most rows of the thin triangles hold no pixel centre.
       const int n_chunks = (n_rows + 31) >> 5;
       if (warp == kWarps - 1 && !prepared) {  // joins the chunk queue afterwards
         prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
                     lane);
         prepared = true;
       }
-      while (true) {
+      uint2 *q = s_queue + warp * 64;
+      int qn = 0;  // queued spans (warp-uniform)
+      bool more = true;
+      while (more) {
         int k = 0;
         if (lane == 0) k = atomicAdd(&es.chunk_next, 1);
         k = __shfl_sync(kFull, k, 0);
-        if (k >= n_chunks) break;
-        const int u = k * 32 + lane;
-        // owner triangle of unit u: the owner of the chunk's first unit plus
-        // the triangles starting inside the chunk up to u (all have >= 1 row)
-        const int o0 = s_rowner[k];
-        const int mi = o0 + 1 + lane;
-        uint32_t bit = 0;
-        if (mi < n_round) {
-          const int d = (int)s_span[mi].row0 - k * 32;  // >= 1
-          if (d < 32) bit = 1u << d;
-        }
-        const uint32_t starts = __reduce_or_sync(kFull, bit);
-        const int j = o0 + __popc(starts & lanemask_le);
-        int len = 0, x0 = 0, row = 0;
-        if (u < n_rows) {
-          const SpanRec &S = s_span[j];
-          row = (int)S.py0 + (u - (int)S.row0);
-          len = row_span(S, row, x0);
-        }
-        // expand the 32 spans into pixel candidates
-        const int incl = warp_incl_scan(len, lane);
-        const int excl = incl - len;
-        const int N = __shfl_sync(kFull, incl, 31);
-        for (int c0 = 0; c0 < N; c0 += 32) {
-          // span lane of candidate c = c0 + lane: the number of lanes whose
-          // inclusive end is <= c (branch-free binary search over the scan)
-          const int c = c0 + lane;
-          int owner = 0;
-#pragma unroll
-          for (int s = 16; s >= 1; s >>= 1) {
-            const int v = __shfl_sync(kFull, incl, owner + s - 1);
-            if (v <= c) owner += s;
+        more = k < n_chunks;
+        if (more) {
+          const int u = k * 32 + lane;
+          // owner triangle of unit u: the owner of the chunk's first unit plus
+          // the triangles starting inside the chunk up to u (all have >= 1 row)
+          const int o0 = s_rowner[k];
+          const int mi = o0 + 1 + lane;
+          uint32_t bit = 0;
+          if (mi < n_round) {
+            const int d = (int)s_span[mi].row0 - k * 32;  // >= 1
+            if (d < 32) bit = 1u << d;
           }
-          const int o_ex = __shfl_sync(kFull, excl, owner & 31);
-          const int o_x0 = __shfl_sync(kFull, x0, owner & 31);
-          const int o_row = __shfl_sync(kFull, row, owner & 31);
-          const int o_tri = __shfl_sync(kFull, j, owner & 31);
-          bool cov = false;
-          uint32_t pix = 0;
-          double z = 0.0;
-          if (c < N) {
-            const int px = o_x0 + (c - o_ex);
-            pix = (uint32_t)(o_row * p.W + px);
-            cov = eval_exact(s_rec[o_tri], px, o_row, s_vxy64, s_viz, z);
+          const uint32_t starts = __reduce_or_sync(kFull, bit);
+          const int j = o0 + __popc(starts & lanemask_le);
+          int len = 0, x0 = 0, row = 0;
+          if (u < n_rows) {
+            const SpanRec &S = s_span[j];
+            row = (int)S.py0 + (u - (int)S.row0);
+            len = row_span(S, row, x0);
           }
-          const uint32_t cm = __ballot_sync(kFull, cov);
-          if (cm == 0u) continue;
-          const int leader = __ffs(cm) - 1;
-          int slot = 0;
-          if (lane == leader) slot = atomicAdd(&es.n_frag, __popc(cm));
-          slot = __shfl_sync(kFull, slot, leader) + __popc(cm & lanemask_lt);
-          if (cov) {
-            const uint32_t zb = __float_as_uint((float)z);
-            if (zb < atomicMin(&s_dbits[pix], zb)) atomicOr(&s_wkey[pix], kDecBit);
-            if (slot < p.frag_limit) {
-              Frag f;
-              f.z = z;
-              f.pix = pix;
-              f.tri = (uint32_t)o_tri;
-              s_frag[slot] = f;
+          const uint32_t sm = __ballot_sync(kFull, len > 0);
+          if (len > 0)
+            q[qn + __popc(sm & lanemask_lt)] =
+                make_uint2((uint32_t)x0 | ((uint32_t)len << 16), (uint32_t)row | ((uint32_t)j << 16));
+          qn += __popc(sm);
+        }
+        while (qn >= 32 || (!more && qn > 0)) {
+          __syncwarp();
+          const int nb = min(qn, 32);
+          qn -= nb;
+          int len = 0, x0 = 0, row = 0, j = 0;
+          if (lane < nb) {
+            const uint2 sp = q[qn + lane];
+            x0 = (int)(sp.x & 0xffffu);
+            len = (int)(sp.x >> 16);
+            row = (int)(sp.y & 0xffffu);
+            j = (int)(sp.y >> 16);
+          }
+          __syncwarp();
+          // expand the 32 spans into pixel candidates
+          const int incl = warp_incl_scan(len, lane);
+          const int excl = incl - len;
+          const int N = __shfl_sync(kFull, incl, 31);
+          for (int c0 = 0; c0 < N; c0 += 32) {
+            // span lane of candidate c = c0 + lane: the number of lanes whose
+            // inclusive end is <= c (branch-free binary search over the scan)
+            const int c = c0 + lane;
+            int owner = 0;
+  #pragma unroll
+            for (int s = 16; s >= 1; s >>= 1) {
+              const int v = __shfl_sync(kFull, incl, owner + s - 1);
+              if (v <= c) owner += s;
+            }
+            const int o_ex = __shfl_sync(kFull, excl, owner & 31);
+            const int o_x0 = __shfl_sync(kFull, x0, owner & 31);
+            const int o_row = __shfl_sync(kFull, row, owner & 31);
+            const int o_tri = __shfl_sync(kFull, j, owner & 31);
+            bool cov = false;
+            uint32_t pix = 0;
+            double z = 0.0;
+            if (c < N) {
+              const int px = o_x0 + (c - o_ex);
+              pix = (uint32_t)(o_row * p.W + px);
+              cov = eval_exact(s_rec[o_tri], px, o_row, s_vxy64, s_viz, z);
+            }
+            const uint32_t cm = __ballot_sync(kFull, cov);
+            if (cm == 0u) continue;
+            const int leader = __ffs(cm) - 1;
+            int slot = 0;
+            if (lane == leader) slot = atomicAdd(&es.n_frag, __popc(cm));
+            slot = __shfl_sync(kFull, slot, leader) + __popc(cm & lanemask_lt);
+            if (cov) {
+              const uint32_t zb = __float_as_uint((float)z);
+              if (zb < atomicMin(&s_dbits[pix], zb)) atomicOr(&s_wkey[pix], kDecBit);
+              if (slot < p.frag_limit) {
+                Frag f;
+                f.z = z;
+                f.pix = pix;
+                f.tri = (uint32_t)o_tri;
+                s_frag[slot] = f;
+              }
             }
           }
         }
