@@ -151,7 +151,7 @@ __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   int o = 0;
   const int npx = p.H * p.W;
   L.link = o;   o += align_up(2 * p.nl * 16, 16);  // double-buffered (prefetch)
-  L.floor = o;  o += align_up((p.W + 2 * p.H) * 8, 16);
+  L.floor = o;  o += align_up((p.W + 3 * p.H) * 8 + p.H * 4, 16);  // rays + per-row t, parity
   L.maps = o;   o += align_up((p.W + p.H) * 4, 16);  // texel byte offsets per row / column
   L.vxy64 = o;  o += align_up(p.nv * 16, 16);
   L.viz = o;    o += align_up(p.nv * 8, 16);
@@ -269,7 +269,7 @@ __device__ __forceinline__ void floor_px(const RenderParams &p, float ex, float 
     if ((double)p.cam[13] <= t && t <= (double)p.cam[14]) {
       const double wx = (double)ex + t * dx;
       const double wy = (double)p.cam[1] + t * dy;
-      const int64_t parity = ((int64_t)floor(wx) + (int64_t)floor(wy)) & 1;
+      const int64_t parity = (__double2ll_rd(wx) + __double2ll_rd(wy)) & 1;
       const uint32_t c = parity == 0 ? 158u : 122u;  // render.py:51-52
       rgb = c | (c << 8) | (c << 16);
       depth = (float)t;
@@ -472,7 +472,9 @@ render_step_kernel(const RenderParams p) {
   __shared__ int s_scan[kWarps];
   const SmemLayout L = smem_layout(p);
   float4 *s_link = reinterpret_cast<float4 *>(smem + L.link);
-  double *s_floor = reinterpret_cast<double *>(smem + L.floor);
+  double *s_floor = reinterpret_cast<double *>(smem + L.floor);  // dx[W], dy[H], dz[H]
+  double *s_ft = s_floor + p.W + 2 * p.H;                          // per-row floor t
+  int *s_fk = reinterpret_cast<int *>(s_ft + p.H);                 // per-row parity / -1
   uint32_t *s_rowmap = reinterpret_cast<uint32_t *>(smem + L.maps);  // rowmap[y] * Wv * 3
   uint32_t *s_colmap = s_rowmap + p.H;                               // colmap[x] * 3
   double2 *s_vxy64 = reinterpret_cast<double2 *>(smem + L.vxy64);
@@ -591,6 +593,25 @@ render_step_kernel(const RenderParams p) {
     bool prepared = env + gridDim.x >= p.batch;  // nothing to prepare for a last env
 
     // ---- phase 1: world transform + projection (render.py:468-481, 350-363)
+    if (p.draw_floor && p.floor_sep) {
+      // separable floor rays: t = -ez / dz and floor(wy) depend on the row
+      // only (render.py:321-334), computed once per row by the last threads
+      // (the ones with a single vertex below)
+      for (int y = kThreads - 1 - tid; y < p.H; y += kThreads) {
+        const double dy = s_floor[p.W + y], dz = s_floor[p.W + p.H + y];
+        double t = 0.0;
+        int k = -1;  // -1: sky; else parity of floor(wy)
+        if (dz < -1e-12) {
+          t = (double)(-ez) / dz;
+          if ((double)p.cam[13] <= t && t <= (double)p.cam[14]) {
+            const double wy = (double)p.cam[1] + t * dy;
+            k = (int)(__double2ll_rd(wy) & 1);
+          }
+        }
+        s_ft[y] = t;
+        s_fk[y] = k;
+      }
+    }
     for (int v = tid; v < p.nv; v += kThreads) {
       const float3 w = world_vertex(p, s_link_cur, v);
       s_world[3 * v + 0] = w.x;
@@ -662,15 +683,18 @@ render_step_kernel(const RenderParams p) {
         const int y = (int)__umulhi((uint32_t)i, p.wmagic), x = i - y * p.W;
         float d = __int_as_float(0x7f800000);
         uint32_t c = kSkyRGB;
-        if (p.draw_floor) {
-          double dx, dy, dz;
-          if (p.floor_sep) {
-            dx = s_floor[x]; dy = s_floor[p.W + y]; dz = s_floor[p.W + p.H + y];
-          } else {
-            const double *r = p.floor_rays + (int64_t)i * 3;
-            dx = r[0]; dy = r[1]; dz = r[2];
+        if (p.draw_floor && p.floor_sep) {
+          const int k = s_fk[y];
+          if (k >= 0) {  // same arithmetic as floor_px with the row terms hoisted
+            const double t = s_ft[y];
+            const double wx = (double)ex + t * s_floor[x];
+            const uint32_t g = ((uint32_t)__double2ll_rd(wx) ^ (uint32_t)k) & 1u ? 122u : 158u;
+            c = g | (g << 8) | (g << 16);
+            d = (float)t;
           }
-          floor_px(p, ex, ez, dx, dy, dz, d, c);
+        } else if (p.draw_floor) {
+          const double *r = p.floor_rays + (int64_t)i * 3;
+          floor_px(p, ex, ez, r[0], r[1], r[2], d, c);
         }
         s_depth[i] = d;
         put_rgb(s_col, (uint32_t)i, c);
