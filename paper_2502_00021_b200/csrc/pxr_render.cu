@@ -92,11 +92,10 @@ static_assert(sizeof(SpanRec) == 48, "SpanRec layout");
 // row | live_tri << 16} until 32 can be evaluated together.
 constexpr int kQueue = 64;
 
-struct Frag {
-  double z;      // f64 depth of the candidate (render.py:450-451)
-  uint32_t pix;  // y * W + x
-  uint32_t tri;  // live index within the round (== triangle order)
-};
+// A covered fragment: uint2 {RN32(z) bits | (z < RN32(z)) << 31, pix | tri << 20}
+// (depths are positive, so the f32 sign bit is free; pix < 2^20 and the
+// live index of the round < 2^12 by the host's limits).
+constexpr int kMaxCap = 4095;
 
 struct RenderParams {
   const float *base_verts;
@@ -165,7 +164,7 @@ __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   L.span = o;   o += align_up(p.cap * (int)sizeof(SpanRec), 16);
   L.rowner = o; o += align_up((p.row_cap / 32 + 2) * 2, 16);
   L.queue = o;  o += kWarps * kQueue * 8;
-  L.frag = o;   o += kFragCap * (int)sizeof(Frag);
+  L.frag = o;   o += kFragCap * 8;
   L.depth = o;  o += align_up(npx * 4, 16);
   L.col = o;    o += align_up(npx * 3, 16);
   L.wkey = o;   o += align_up(npx * 4, 16);
@@ -489,7 +488,7 @@ render_step_kernel(const RenderParams p) {
   SpanRec *s_span = reinterpret_cast<SpanRec *>(smem + L.span);
   uint16_t *s_rowner = reinterpret_cast<uint16_t *>(smem + L.rowner);
   uint2 *s_queue = reinterpret_cast<uint2 *>(smem + L.queue);
-  Frag *s_frag = reinterpret_cast<Frag *>(smem + L.frag);
+  uint2 *s_frag = reinterpret_cast<uint2 *>(smem + L.frag);
   float *s_depth = reinterpret_cast<float *>(smem + L.depth);
   uint32_t *s_dbits = reinterpret_cast<uint32_t *>(smem + L.depth);
   uint8_t *s_col = smem + L.col;
@@ -651,16 +650,9 @@ render_step_kernel(const RenderParams p) {
           int bx0, bx1, by0, by1;
           pixel_range(minx, maxx, p.W - 1, bx0, bx1);
           pixel_range(miny, maxy, p.H - 1, by0, by1);
-          if (!(bx0 > bx1 || by0 > by1)) {
-            const float *w0 = s_world + 3 * i0, *w1 = s_world + 3 * i1, *w2 = s_world + 3 * i2;
-            const float e1x = w1[0] - w0[0], e1y = w1[1] - w0[1], e1z = w1[2] - w0[2];
-            const float e2x = w2[0] - w0[0], e2y = w2[1] - w0[1], e2z = w2[2] - w0[2];
-            const float nx = e1y * e2z - e1z * e2y;
-            const float ny = e1z * e2x - e1x * e2z;
-            const float nz = e1x * e2y - e1y * e2x;
-            if (!((double)sqrtf(nx * nx + ny * ny + nz * nz) < 1e-20))
-              rows = (uint32_t)(by1 - by0 + 1);
-          }
+          // (the degenerate-normal cull, render.py:405-409, is applied by
+          // the records phase, which computes the normal for the shading)
+          if (!(bx0 > bx1 || by0 > by1)) rows = (uint32_t)(by1 - by0 + 1);
         }
       }
       s_rows[t] = (uint16_t)rows;
@@ -819,8 +811,9 @@ render_step_kernel(const RenderParams p) {
         s_rec[li - r0] = R;
         SpanRec S;
         span_setup(a, b, c, (float)(p.H + 1), S);
-        S.px0 = (uint16_t)bx0;
-        S.px1 = (uint16_t)bx1;
+        const bool culled = (double)nn < 1e-20;  // degenerate normal (render.py:405-409)
+        S.px0 = (uint16_t)(culled ? 1 : bx0);    // culled: every row span is empty
+        S.px1 = (uint16_t)(culled ? 0 : bx1);
         S.py0 = (uint16_t)by0;
         const uint32_t u0 = s_lrp[li] - rbase;
         S.row0 = u0;
@@ -922,15 +915,12 @@ render_step_kernel(const RenderParams p) {
             if (lane == leader) slot = atomicAdd(&es.n_frag, __popc(cm));
             slot = __shfl_sync(kFull, slot, leader) + __popc(cm & lanemask_lt);
             if (cov) {
-              const uint32_t zb = __float_as_uint((float)z);
+              const float zf = (float)z;
+              const uint32_t zb = __float_as_uint(zf);
               if (zb < atomicMin(&s_dbits[pix], zb)) atomicOr(&s_wkey[pix], kDecBit);
-              if (slot < p.frag_limit) {
-                Frag f;
-                f.z = z;
-                f.pix = pix;
-                f.tri = (uint32_t)o_tri;
-                s_frag[slot] = f;
-              }
+              if (slot < p.frag_limit)
+                s_frag[slot] = make_uint2(zb | (z < (double)zf ? 0x80000000u : 0u),
+                                          pix | ((uint32_t)o_tri << 20));
             }
           }
         }
@@ -941,23 +931,21 @@ render_step_kernel(const RenderParams p) {
       const int n_frag = es.n_frag;
       if (n_frag <= p.frag_limit) {
         for (int i = tid; i < n_frag; i += kThreads) {
-          const Frag f = s_frag[i];
-          const uint32_t F = s_dbits[f.pix];
-          if (__float_as_uint((float)f.z) == F) {
-            const uint32_t hb = s_wkey[f.pix] & kDecBit;  // stable after the barrier
-            atomicMax(&s_wkey[f.pix],
-                      hb | (f.z < (double)__uint_as_float(F) ? 0x10000u + f.tri
-                                                             : 0xFFFFu - f.tri));
+          const uint2 f = s_frag[i];
+          const uint32_t pix = f.y & 0xFFFFFu, tri = f.y >> 20;
+          if ((f.x & 0x7FFFFFFFu) == s_dbits[pix]) {  // in S: z < F == z < RN32(z)
+            const uint32_t hb = s_wkey[pix] & kDecBit;  // stable after the barrier
+            atomicMax(&s_wkey[pix], hb | ((f.x >> 31) ? 0x10000u + tri : 0xFFFFu - tri));
           }
         }
         __syncthreads();
         for (int i = tid; i < n_frag; i += kThreads) {
-          const Frag f = s_frag[i];
-          if (resolve_winner(s_wkey[f.pix]) == (int)f.tri) put_rgb(s_col, f.pix, s_rec[f.tri].rgb);
+          const uint32_t pix = s_frag[i].y & 0xFFFFFu, tri = s_frag[i].y >> 20;
+          if (resolve_winner(s_wkey[pix]) == (int)tri) put_rgb(s_col, pix, s_rec[tri].rgb);
         }
         if (r1 < n_live) {
           __syncthreads();
-          for (int i = tid; i < n_frag; i += kThreads) s_wkey[s_frag[i].pix] = 0u;
+          for (int i = tid; i < n_frag; i += kThreads) s_wkey[s_frag[i].y & 0xFFFFFu] = 0u;
         }
       } else {
         // fragment list overflow: recompute the candidates for both passes
@@ -1323,7 +1311,7 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
       max_optin - (int)(sizeof(EnvShared) + sizeof(DistSlot) * 32 + 4 * kWarps) - 256;
   // Live-triangle records per round: all triangles if they fit, else the
   // largest count that does (extra rounds handle the rest exactly).
-  int cap = p.nt > 0 ? p.nt : 1;
+  int cap = p.nt > 0 ? (p.nt < kMaxCap ? p.nt : kMaxCap) : 1;
   if (debug_cap > 0 && debug_cap < cap) cap = debug_cap;
   for (;;) {
     p.cap = cap;
