@@ -13,7 +13,8 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpxr.so")
+# PXR_LIB_PATH: load another build of the same ABI (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("PXR_LIB_PATH") or os.path.join(_HERE, "libpxr.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 PXR_OK = 0

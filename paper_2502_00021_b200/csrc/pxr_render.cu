@@ -136,6 +136,7 @@ struct RenderParams {
   uint32_t wmagic;  // ceil(2^32 / W): flat pixel index -> row
   uint32_t gmagic;  // ceil(2^32 / (W / 4)): 4-pixel group -> row (W % 4 == 0)
   int depth_vec;    // out_depth groups of 4 pixels are 16-byte aligned
+  int band_h;       // rows per band: a frame is rendered in bands that fit shared memory
 };
 
 struct SmemLayout {
@@ -148,7 +149,7 @@ __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a *
 __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   SmemLayout L;
   int o = 0;
-  const int npx = p.H * p.W;
+  const int npx = p.band_h * p.W;  // per-pixel arrays hold one band
   L.link = o;   o += align_up(2 * p.nl * 16, 16);  // double-buffered (prefetch)
   L.floor = o;  o += align_up((p.W + 3 * p.H) * 8 + p.H * 4, 16);  // rays + per-row t, parity
   L.maps = o;   o += align_up((p.W + p.H) * 4, 16);  // texel byte offsets per row / column
@@ -463,6 +464,8 @@ __device__ __forceinline__ void put_texel(uint32_t w[3], int k, uint32_t t) {
   }
 }
 
+// kBands = false: the whole frame is one band (y0 = 0, straight-line code).
+template <bool kBands>
 __global__ void __launch_bounds__(kThreads, 1)
 render_step_kernel(const RenderParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -501,7 +504,8 @@ render_step_kernel(const RenderParams p) {
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int npx = p.H * p.W;
+  const int fpx = p.H * p.W;  // pixels per frame
+  const int chans = p.gray ? 1 : 3;
   const double aspect = (double)p.W / (double)p.H;  // render.py:303
   const float ey = p.cam[1];
   const float rx = p.cam[3], ry = p.cam[4], rz = p.cam[5];
@@ -635,485 +639,510 @@ render_step_kernel(const RenderParams p) {
     if (tid == 0 && p.use_bulk) bulk_wait_read();
     __syncthreads();
 
-    // ---- phase 2: liveness (render.py:366-416) + background -------------
-    for (int t = tid; t < p.nt; t += kThreads) {
-      uint32_t rows = 0;
-      const int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
-                i2 = __ldg(p.tris + 3 * t + 2);
-      const float z0 = s_vz[i0], z1 = s_vz[i1], z2 = s_vz[i2];
-      if (!(z0 < near_ || z1 < near_ || z2 < near_) && !(z0 > far_ && z1 > far_ && z2 > far_)) {
-        const float2 a = s_vxy32[i0], b = s_vxy32[i1], c = s_vxy32[i2];
-        const float area2 = (b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x);
-        if (area2 != 0.0f) {
+    // ---- bands of rows: everything below runs once per band (one band
+    // whenever the frame's per-pixel state fits shared memory) ------------
+    const int band_h = kBands ? p.band_h : p.H;
+    int yb = 0;
+    do {  // (no loop at all for one band)
+      const int y0 = kBands ? yb : 0;  // compile-time 0 for one band
+      const int y1 = kBands ? min(y0 + band_h, p.H) : p.H;
+      const int npx = (y1 - y0) * p.W;  // pixels of this band
+      if (kBands && y0 > 0) {  // the previous band's TMA store must have finished reading
+        if (tid == 0 && p.use_bulk) bulk_wait_read();
+        __syncthreads();
+      }
+
+      // ---- phase 2: liveness (render.py:366-416) + background -------------
+      for (int t = tid; t < p.nt; t += kThreads) {
+        uint32_t rows = 0;
+        const int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
+                  i2 = __ldg(p.tris + 3 * t + 2);
+        const float z0 = s_vz[i0], z1 = s_vz[i1], z2 = s_vz[i2];
+        if (!(z0 < near_ || z1 < near_ || z2 < near_) && !(z0 > far_ && z1 > far_ && z2 > far_)) {
+          const float2 a = s_vxy32[i0], b = s_vxy32[i1], c = s_vxy32[i2];
+          const float area2 = (b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x);
+          if (area2 != 0.0f) {
+            const float minx = fminf(a.x, fminf(b.x, c.x)), maxx = fmaxf(a.x, fmaxf(b.x, c.x));
+            const float miny = fminf(a.y, fminf(b.y, c.y)), maxy = fmaxf(a.y, fmaxf(b.y, c.y));
+            int bx0, bx1, by0, by1;
+            pixel_range(minx, maxx, p.W - 1, bx0, bx1);
+            pixel_range(miny, maxy, p.H - 1, by0, by1);
+            by0 = max(by0, y0);  // this band's rows only
+            by1 = min(by1, y1 - 1);
+            // (the degenerate-normal cull, render.py:405-409, is applied by
+            // the records phase, which computes the normal for the shading)
+            if (!(bx0 > bx1 || by0 > by1)) rows = (uint32_t)(by1 - by0 + 1);
+          }
+        }
+        s_rows[t] = (uint16_t)rows;
+      }
+      // background: sky / floor under an empty z-buffer (render.py:306-344)
+      if (p.mode == PXR_MODE_VIDEO && !p.draw_floor) {
+        // the background colour is never read: every inf pixel takes the video
+        const float inf = __int_as_float(0x7f800000);
+        const int n4 = npx >> 2;
+        for (int i = tid; i < n4; i += kThreads) {
+          reinterpret_cast<float4 *>(s_depth)[i] = make_float4(inf, inf, inf, inf);
+          reinterpret_cast<uint4 *>(s_wkey)[i] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        for (int i = (n4 << 2) + tid; i < npx; i += kThreads) {
+          s_depth[i] = inf;
+          s_wkey[i] = 0u;
+        }
+      } else {
+        for (int i = tid; i < npx; i += kThreads) {
+          const int yb = (int)__umulhi((uint32_t)i, p.wmagic), x = i - yb * p.W;
+          const int y = y0 + yb;
+          float d = __int_as_float(0x7f800000);
+          uint32_t c = kSkyRGB;
+          if (p.draw_floor && p.floor_sep) {
+            const int k = s_fk[y];
+            if (k >= 0) {  // same arithmetic as floor_px with the row terms hoisted
+              const double t = s_ft[y];
+              const double wx = (double)ex + t * s_floor[x];
+              const uint32_t g = ((uint32_t)__double2ll_rd(wx) ^ (uint32_t)k) & 1u ? 122u : 158u;
+              c = g | (g << 8) | (g << 16);
+              d = (float)t;
+            }
+          } else if (p.draw_floor) {
+            const double *r = p.floor_rays + ((int64_t)y0 * p.W + i) * 3;
+            floor_px(p, ex, ez, r[0], r[1], r[2], d, c);
+          }
+          s_depth[i] = d;
+          put_rgb(s_col, (uint32_t)i, c);
+          s_wkey[i] = 0u;
+        }
+      }
+      __syncthreads();
+      // block scan over triangles in index order: live ids, bbox-row prefix
+      {
+        const int per = (p.nt + kThreads - 1) / kThreads;
+        const int t0 = min(tid * per, p.nt), t1 = min(t0 + per, p.nt);
+        int nlive = 0, nrows = 0;
+        for (int t = t0; t < t1; t++) {
+          const int r = s_rows[t];
+          nlive += r != 0;
+          nrows += r;
+        }
+        const int packed = nlive | (nrows << 12);  // per <= 128 < 2^12 live
+        const int wincl = warp_incl_scan(packed, lane);
+        if (lane == 31) s_scan[warp] = wincl;
+        __syncthreads();
+        if (warp == 0) {
+          const int v = lane < kWarps ? s_scan[lane] : 0;
+          const int vi = warp_incl_scan(v, lane);
+          if (lane < kWarps) s_scan[lane] = vi - v;
+          if (lane == kWarps - 1) es.n_live = vi & 0xfff;
+        }
+        __syncthreads();
+        const int base = s_scan[warp] + wincl - packed;
+        int li = base & 0xfff;
+        uint32_t racc = (uint32_t)base >> 12;
+        for (int t = t0; t < t1; t++) {
+          const int r = s_rows[t];
+          if (r != 0) {
+            s_ids[li] = (uint16_t)t;
+            s_lrp[li] = racc;
+            li++;
+            racc += (uint32_t)r;
+          }
+        }
+        if (tid == kThreads - 1) s_lrp[li] = racc;  // the last thread holds the totals
+      }
+      __syncthreads();
+      const int n_live = es.n_live;
+
+      // ---- phases 3/4: raster rounds over live triangles in index order ---
+      for (int r0 = 0; r0 < n_live;) {
+        if (tid == 0) {
+          // live [r0, r1): at most cap triangles and row_cap bbox rows (a
+          // single triangle always fits: row_cap >= H); when several rounds
+          // are needed their triangle counts are balanced (a small last round
+          // cannot fill the CTA)
+          const int left = n_live - r0;
+          const int n_rounds = (left + p.cap - 1) / p.cap;
+          const int target = (left + n_rounds - 1) / n_rounds;
+          int lo = r0 + 1, hi = min(r0 + target, n_live);
+          const uint32_t base = s_lrp[r0];
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_lrp[mid] - base <= (uint32_t)p.row_cap) lo = mid; else hi = mid - 1;
+          }
+          es.round_end = lo;
+          es.chunk_next = 0;
+          es.n_frag = 0;
+        }
+        __syncthreads();
+        const int r1 = es.round_end;
+        const uint32_t rbase = s_lrp[r0];
+        const int n_rows = (int)(s_lrp[r1] - rbase);
+        const int n_round = r1 - r0;
+        // records (render.py:366-436), span line equations, row-chunk owners
+        for (int li = r0 + tid; li < r1; li += kThreads) {
+          const int t = s_ids[li];
+          int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
+              i2 = __ldg(p.tris + 3 * t + 2);
+          const float2 a = s_vxy32[i0];
+          float2 b = s_vxy32[i1], c = s_vxy32[i2];
+          float area2 = (b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x);
+          // flat Lambert from the UNswapped world-space normal (render.py:405-423)
+          const float *w0 = s_world + 3 * i0, *w1 = s_world + 3 * i1, *w2 = s_world + 3 * i2;
+          const float e1x = w1[0] - w0[0], e1y = w1[1] - w0[1], e1z = w1[2] - w0[2];
+          const float e2x = w2[0] - w0[0], e2y = w2[1] - w0[1], e2z = w2[2] - w0[2];
+          const float nx = e1y * e2z - e1z * e2y;
+          const float ny = e1z * e2x - e1x * e2z;
+          const float nz = e1x * e2y - e1y * e2x;
+          const float nn = sqrtf(nx * nx + ny * ny + nz * nz);
+          const float nd32 = (nx * lx + ny * ly + nz * lz) / nn;
+          const double ndotl = nd32 < 0.0f ? 0.0 : (double)nd32;
+          const double shade = 0.35 + 0.65 * ndotl;
+          uint32_t rgb = 0;
+          for (int ch = 0; ch < 3; ch++) {
+            double v = (double)__ldg(p.tri_colors + 3 * t + ch) * shade * 255.0;
+            if (v > 255.0) v = 255.0;
+            rgb |= ((uint32_t)v & 0xffu) << (8 * ch);
+          }
+          if (area2 < 0.0f) {  // swap v1 <-> v2 (render.py:381-385)
+            const float2 tmp = b; b = c; c = tmp;
+            const int ti = i1; i1 = i2; i2 = ti;
+            area2 = -area2;
+          }
           const float minx = fminf(a.x, fminf(b.x, c.x)), maxx = fmaxf(a.x, fmaxf(b.x, c.x));
           const float miny = fminf(a.y, fminf(b.y, c.y)), maxy = fmaxf(a.y, fmaxf(b.y, c.y));
           int bx0, bx1, by0, by1;
           pixel_range(minx, maxx, p.W - 1, bx0, bx1);
           pixel_range(miny, maxy, p.H - 1, by0, by1);
-          // (the degenerate-normal cull, render.py:405-409, is applied by
-          // the records phase, which computes the normal for the shading)
-          if (!(bx0 > bx1 || by0 > by1)) rows = (uint32_t)(by1 - by0 + 1);
-        }
-      }
-      s_rows[t] = (uint16_t)rows;
-    }
-    // background: sky / floor under an empty z-buffer (render.py:306-344)
-    if (p.mode == PXR_MODE_VIDEO && !p.draw_floor) {
-      // the background colour is never read: every inf pixel takes the video
-      const float inf = __int_as_float(0x7f800000);
-      const int n4 = npx >> 2;
-      for (int i = tid; i < n4; i += kThreads) {
-        reinterpret_cast<float4 *>(s_depth)[i] = make_float4(inf, inf, inf, inf);
-        reinterpret_cast<uint4 *>(s_wkey)[i] = make_uint4(0u, 0u, 0u, 0u);
-      }
-      for (int i = (n4 << 2) + tid; i < npx; i += kThreads) {
-        s_depth[i] = inf;
-        s_wkey[i] = 0u;
-      }
-    } else {
-      for (int i = tid; i < npx; i += kThreads) {
-        const int y = (int)__umulhi((uint32_t)i, p.wmagic), x = i - y * p.W;
-        float d = __int_as_float(0x7f800000);
-        uint32_t c = kSkyRGB;
-        if (p.draw_floor && p.floor_sep) {
-          const int k = s_fk[y];
-          if (k >= 0) {  // same arithmetic as floor_px with the row terms hoisted
-            const double t = s_ft[y];
-            const double wx = (double)ex + t * s_floor[x];
-            const uint32_t g = ((uint32_t)__double2ll_rd(wx) ^ (uint32_t)k) & 1u ? 122u : 158u;
-            c = g | (g << 8) | (g << 16);
-            d = (float)t;
-          }
-        } else if (p.draw_floor) {
-          const double *r = p.floor_rays + (int64_t)i * 3;
-          floor_px(p, ex, ez, r[0], r[1], r[2], d, c);
-        }
-        s_depth[i] = d;
-        put_rgb(s_col, (uint32_t)i, c);
-        s_wkey[i] = 0u;
-      }
-    }
-    __syncthreads();
-    // block scan over triangles in index order: live ids, bbox-row prefix
-    {
-      const int per = (p.nt + kThreads - 1) / kThreads;
-      const int t0 = min(tid * per, p.nt), t1 = min(t0 + per, p.nt);
-      int nlive = 0, nrows = 0;
-      for (int t = t0; t < t1; t++) {
-        const int r = s_rows[t];
-        nlive += r != 0;
-        nrows += r;
-      }
-      const int packed = nlive | (nrows << 12);  // per <= 128 < 2^12 live
-      const int wincl = warp_incl_scan(packed, lane);
-      if (lane == 31) s_scan[warp] = wincl;
-      __syncthreads();
-      if (warp == 0) {
-        const int v = lane < kWarps ? s_scan[lane] : 0;
-        const int vi = warp_incl_scan(v, lane);
-        if (lane < kWarps) s_scan[lane] = vi - v;
-        if (lane == kWarps - 1) es.n_live = vi & 0xfff;
-      }
-      __syncthreads();
-      const int base = s_scan[warp] + wincl - packed;
-      int li = base & 0xfff;
-      uint32_t racc = (uint32_t)base >> 12;
-      for (int t = t0; t < t1; t++) {
-        const int r = s_rows[t];
-        if (r != 0) {
-          s_ids[li] = (uint16_t)t;
-          s_lrp[li] = racc;
-          li++;
-          racc += (uint32_t)r;
-        }
-      }
-      if (tid == kThreads - 1) s_lrp[li] = racc;  // the last thread holds the totals
-    }
-    __syncthreads();
-    const int n_live = es.n_live;
-
-    // ---- phases 3/4: raster rounds over live triangles in index order ---
-    for (int r0 = 0; r0 < n_live;) {
-      if (tid == 0) {
-        // live [r0, r1): at most cap triangles and row_cap bbox rows (a
-        // single triangle always fits: row_cap >= H); when several rounds
-        // are needed their triangle counts are balanced (a small last round
-        // cannot fill the CTA)
-        const int left = n_live - r0;
-        const int n_rounds = (left + p.cap - 1) / p.cap;
-        const int target = (left + n_rounds - 1) / n_rounds;
-        int lo = r0 + 1, hi = min(r0 + target, n_live);
-        const uint32_t base = s_lrp[r0];
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (s_lrp[mid] - base <= (uint32_t)p.row_cap) lo = mid; else hi = mid - 1;
-        }
-        es.round_end = lo;
-        es.chunk_next = 0;
-        es.n_frag = 0;
-      }
-      __syncthreads();
-      const int r1 = es.round_end;
-      const uint32_t rbase = s_lrp[r0];
-      const int n_rows = (int)(s_lrp[r1] - rbase);
-      const int n_round = r1 - r0;
-      // records (render.py:366-436), span line equations, row-chunk owners
-      for (int li = r0 + tid; li < r1; li += kThreads) {
-        const int t = s_ids[li];
-        int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
-            i2 = __ldg(p.tris + 3 * t + 2);
-        const float2 a = s_vxy32[i0];
-        float2 b = s_vxy32[i1], c = s_vxy32[i2];
-        float area2 = (b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x);
-        // flat Lambert from the UNswapped world-space normal (render.py:405-423)
-        const float *w0 = s_world + 3 * i0, *w1 = s_world + 3 * i1, *w2 = s_world + 3 * i2;
-        const float e1x = w1[0] - w0[0], e1y = w1[1] - w0[1], e1z = w1[2] - w0[2];
-        const float e2x = w2[0] - w0[0], e2y = w2[1] - w0[1], e2z = w2[2] - w0[2];
-        const float nx = e1y * e2z - e1z * e2y;
-        const float ny = e1z * e2x - e1x * e2z;
-        const float nz = e1x * e2y - e1y * e2x;
-        const float nn = sqrtf(nx * nx + ny * ny + nz * nz);
-        const float nd32 = (nx * lx + ny * ly + nz * lz) / nn;
-        const double ndotl = nd32 < 0.0f ? 0.0 : (double)nd32;
-        const double shade = 0.35 + 0.65 * ndotl;
-        uint32_t rgb = 0;
-        for (int ch = 0; ch < 3; ch++) {
-          double v = (double)__ldg(p.tri_colors + 3 * t + ch) * shade * 255.0;
-          if (v > 255.0) v = 255.0;
-          rgb |= ((uint32_t)v & 0xffu) << (8 * ch);
-        }
-        if (area2 < 0.0f) {  // swap v1 <-> v2 (render.py:381-385)
-          const float2 tmp = b; b = c; c = tmp;
-          const int ti = i1; i1 = i2; i2 = ti;
-          area2 = -area2;
-        }
-        const float minx = fminf(a.x, fminf(b.x, c.x)), maxx = fmaxf(a.x, fmaxf(b.x, c.x));
-        const float miny = fminf(a.y, fminf(b.y, c.y)), maxy = fmaxf(a.y, fmaxf(b.y, c.y));
-        int bx0, bx1, by0, by1;
-        pixel_range(minx, maxx, p.W - 1, bx0, bx1);
-        pixel_range(miny, maxy, p.H - 1, by0, by1);
-        const float ax0 = b.x - a.x, ay0 = b.y - a.y;
-        const float ax1 = c.x - b.x, ay1 = c.y - b.y;
-        const float ax2 = a.x - c.x, ay2 = a.y - c.y;
-        uint32_t fl = 0;
-        if (ay0 < 0.0f || (ay0 == 0.0f && ax0 > 0.0f)) fl |= 1u;
-        if (ay1 < 0.0f || (ay1 == 0.0f && ax1 > 0.0f)) fl |= 2u;
-        if (ay2 < 0.0f || (ay2 == 0.0f && ax2 > 0.0f)) fl |= 4u;
-        TriRec R;
-        R.A0 = ax0; R.B0 = ay0;
-        R.A1 = ax1; R.B1 = ay1;
-        R.A2 = ax2; R.B2 = ay2;
-        R.area = area2;
-        R.rgb = rgb;
-        R.rcp = __drcp_rn((double)area2);
-        R.v0 = (uint16_t)i0; R.v1 = (uint16_t)i1; R.v2 = (uint16_t)i2;
-        R.flags = (uint16_t)fl;
-        s_rec[li - r0] = R;
-        SpanRec S;
-        span_setup(a, b, c, (float)(p.H + 1), S);
-        const bool culled = (double)nn < 1e-20;  // degenerate normal (render.py:405-409)
-        S.px0 = (uint16_t)(culled ? 1 : bx0);    // culled: every row span is empty
-        S.px1 = (uint16_t)(culled ? 0 : bx1);
-        S.py0 = (uint16_t)by0;
-        const uint32_t u0 = s_lrp[li] - rbase;
-        S.row0 = u0;
-        s_span[li - r0] = S;
-        const uint32_t u1 = u0 + (uint32_t)(by1 - by0 + 1);
-        for (uint32_t k = (u0 + 31) >> 5; k <= ((u1 - 1) >> 5); k++)
-          s_rowner[k] = (uint16_t)(li - r0);
-      }
-      __syncthreads();
-
-      // (triangle, bbox row) units, 32 per chunk, chunks scheduled
-      // dynamically: each lane computes one row's conservative span and the
-      // non-empty spans go to the warp's queue; whenever 32 are queued (and
-      // at the end) the warp expands 32 spans into pixel candidates and runs
-      // the exact test on them, so the f64 work runs on full warps even
-      // though most rows of the thin triangles hold no pixel centre.
-      const int n_chunks = (n_rows + 31) >> 5;
-      if (warp == kWarps - 1 && !prepared) {  // joins the chunk queue afterwards
-        prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
-                    lane);
-        prepared = true;
-      }
-      uint2 *q = s_queue + warp * 64;
-      int qn = 0;  // queued spans (warp-uniform)
-      bool more = true;
-      while (more) {
-        int k = 0;
-        if (lane == 0) k = atomicAdd(&es.chunk_next, 1);
-        k = __shfl_sync(kFull, k, 0);
-        more = k < n_chunks;
-        if (more) {
-          const int u = k * 32 + lane;
-          // owner triangle of unit u: the owner of the chunk's first unit plus
-          // the triangles starting inside the chunk up to u (all have >= 1 row)
-          const int o0 = s_rowner[k];
-          const int mi = o0 + 1 + lane;
-          uint32_t bit = 0;
-          if (mi < n_round) {
-            const int d = (int)s_span[mi].row0 - k * 32;  // >= 1
-            if (d < 32) bit = 1u << d;
-          }
-          const uint32_t starts = __reduce_or_sync(kFull, bit);
-          const int j = o0 + __popc(starts & lanemask_le);
-          int len = 0, x0 = 0, row = 0;
-          if (u < n_rows) {
-            const SpanRec &S = s_span[j];
-            row = (int)S.py0 + (u - (int)S.row0);
-            len = row_span(S, row, x0);
-          }
-          const uint32_t sm = __ballot_sync(kFull, len > 0);
-          if (len > 0)
-            q[qn + __popc(sm & lanemask_lt)] =
-                make_uint2((uint32_t)x0 | ((uint32_t)len << 16), (uint32_t)row | ((uint32_t)j << 16));
-          qn += __popc(sm);
-        }
-        while (qn >= 32 || (!more && qn > 0)) {
-          __syncwarp();
-          const int nb = min(qn, 32);
-          qn -= nb;
-          int len = 0, x0 = 0, row = 0, j = 0;
-          if (lane < nb) {
-            const uint2 sp = q[qn + lane];
-            x0 = (int)(sp.x & 0xffffu);
-            len = (int)(sp.x >> 16);
-            row = (int)(sp.y & 0xffffu);
-            j = (int)(sp.y >> 16);
-          }
-          __syncwarp();
-          // expand the 32 spans into pixel candidates
-          const int incl = warp_incl_scan(len, lane);
-          const int excl = incl - len;
-          const int N = __shfl_sync(kFull, incl, 31);
-          for (int c0 = 0; c0 < N; c0 += 32) {
-            // span lane of candidate c = c0 + lane: the number of lanes whose
-            // inclusive end is <= c (branch-free binary search over the scan)
-            const int c = c0 + lane;
-            int owner = 0;
-  #pragma unroll
-            for (int s = 16; s >= 1; s >>= 1) {
-              const int v = __shfl_sync(kFull, incl, owner + s - 1);
-              if (v <= c) owner += s;
-            }
-            const int o_ex = __shfl_sync(kFull, excl, owner & 31);
-            const int o_x0 = __shfl_sync(kFull, x0, owner & 31);
-            const int o_row = __shfl_sync(kFull, row, owner & 31);
-            const int o_tri = __shfl_sync(kFull, j, owner & 31);
-            bool cov = false;
-            uint32_t pix = 0;
-            double z = 0.0;
-            if (c < N) {
-              const int px = o_x0 + (c - o_ex);
-              pix = (uint32_t)(o_row * p.W + px);
-              cov = eval_exact(s_rec[o_tri], px, o_row, s_vxy64, s_viz, z);
-            }
-            const uint32_t cm = __ballot_sync(kFull, cov);
-            if (cm == 0u) continue;
-            const int leader = __ffs(cm) - 1;
-            int slot = 0;
-            if (lane == leader) slot = atomicAdd(&es.n_frag, __popc(cm));
-            slot = __shfl_sync(kFull, slot, leader) + __popc(cm & lanemask_lt);
-            if (cov) {
-              const float zf = (float)z;
-              const uint32_t zb = __float_as_uint(zf);
-              if (zb < atomicMin(&s_dbits[pix], zb)) atomicOr(&s_wkey[pix], kDecBit);
-              if (slot < p.frag_limit)
-                s_frag[slot] = make_uint2(zb | (z < (double)zf ? 0x80000000u : 0u),
-                                          pix | ((uint32_t)o_tri << 20));
-            }
-          }
-        }
-      }
-      __syncthreads();
-
-      // exact sequential-order resolve (see the file header)
-      const int n_frag = es.n_frag;
-      if (n_frag <= p.frag_limit) {
-        for (int i = tid; i < n_frag; i += kThreads) {
-          const uint2 f = s_frag[i];
-          const uint32_t pix = f.y & 0xFFFFFu, tri = f.y >> 20;
-          if ((f.x & 0x7FFFFFFFu) == s_dbits[pix]) {  // in S: z < F == z < RN32(z)
-            const uint32_t hb = s_wkey[pix] & kDecBit;  // stable after the barrier
-            atomicMax(&s_wkey[pix], hb | ((f.x >> 31) ? 0x10000u + tri : 0xFFFFu - tri));
-          }
+          by0 = max(by0, y0);
+          by1 = min(by1, y1 - 1);
+          const float ax0 = b.x - a.x, ay0 = b.y - a.y;
+          const float ax1 = c.x - b.x, ay1 = c.y - b.y;
+          const float ax2 = a.x - c.x, ay2 = a.y - c.y;
+          uint32_t fl = 0;
+          if (ay0 < 0.0f || (ay0 == 0.0f && ax0 > 0.0f)) fl |= 1u;
+          if (ay1 < 0.0f || (ay1 == 0.0f && ax1 > 0.0f)) fl |= 2u;
+          if (ay2 < 0.0f || (ay2 == 0.0f && ax2 > 0.0f)) fl |= 4u;
+          TriRec R;
+          R.A0 = ax0; R.B0 = ay0;
+          R.A1 = ax1; R.B1 = ay1;
+          R.A2 = ax2; R.B2 = ay2;
+          R.area = area2;
+          R.rgb = rgb;
+          R.rcp = __drcp_rn((double)area2);
+          R.v0 = (uint16_t)i0; R.v1 = (uint16_t)i1; R.v2 = (uint16_t)i2;
+          R.flags = (uint16_t)fl;
+          s_rec[li - r0] = R;
+          SpanRec S;
+          span_setup(a, b, c, (float)(p.H + 1), S);
+          const bool culled = (double)nn < 1e-20;  // degenerate normal (render.py:405-409)
+          S.px0 = (uint16_t)(culled ? 1 : bx0);    // culled: every row span is empty
+          S.px1 = (uint16_t)(culled ? 0 : bx1);
+          S.py0 = (uint16_t)by0;
+          const uint32_t u0 = s_lrp[li] - rbase;
+          S.row0 = u0;
+          s_span[li - r0] = S;
+          const uint32_t u1 = u0 + (uint32_t)(by1 - by0 + 1);
+          for (uint32_t k = (u0 + 31) >> 5; k <= ((u1 - 1) >> 5); k++)
+            s_rowner[k] = (uint16_t)(li - r0);
         }
         __syncthreads();
-        for (int i = tid; i < n_frag; i += kThreads) {
-          const uint32_t pix = s_frag[i].y & 0xFFFFFu, tri = s_frag[i].y >> 20;
-          if (resolve_winner(s_wkey[pix]) == (int)tri) put_rgb(s_col, pix, s_rec[tri].rgb);
+
+        // (triangle, bbox row) units, 32 per chunk, chunks scheduled
+        // dynamically: each lane computes one row's conservative span and the
+        // non-empty spans go to the warp's queue; whenever 32 are queued (and
+        // at the end) the warp expands 32 spans into pixel candidates and runs
+        // the exact test on them, so the f64 work runs on full warps even
+        // though most rows of the thin triangles hold no pixel centre.
+        const int n_chunks = (n_rows + 31) >> 5;
+        if (warp == kWarps - 1 && !prepared) {  // joins the chunk queue afterwards
+          prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
+                      lane);
+          prepared = true;
         }
-        if (r1 < n_live) {
-          __syncthreads();
-          for (int i = tid; i < n_frag; i += kThreads) s_wkey[s_frag[i].y & 0xFFFFFu] = 0u;
-        }
-      } else {
-        // fragment list overflow: recompute the candidates for both passes
-        for (int pass = 0; pass < 2; pass++) {
-          for (int u = tid; u < n_rows; u += kThreads) {
-            int j = s_rowner[u >> 5];
-            while (j + 1 < n_round && s_span[j + 1].row0 <= (uint32_t)u) j++;
-            const SpanRec &S = s_span[j];
-            const TriRec &R = s_rec[j];
-            const int row = (int)S.py0 + (u - (int)S.row0);
-            int x0;
-            const int len = row_span(S, row, x0);
-            for (int px = x0; px < x0 + len; px++) {
-              double z;
-              if (!eval_exact(R, px, row, s_vxy64, s_viz, z)) continue;
-              const uint32_t pix = (uint32_t)(row * p.W + px);
-              const uint32_t F = s_dbits[pix];
-              if (__float_as_uint((float)z) != F) continue;
-              if (pass == 0) {
-                const uint32_t hb = s_wkey[pix] & kDecBit;
-                atomicMax(&s_wkey[pix],
-                          hb | (z < (double)__uint_as_float(F) ? 0x10000u + j : 0xFFFFu - j));
-              } else if (resolve_winner(s_wkey[pix]) == j) {
-                put_rgb(s_col, pix, R.rgb);
+        uint2 *q = s_queue + warp * 64;
+        int qn = 0;  // queued spans (warp-uniform)
+        bool more = true;
+        while (more) {
+          int k = 0;
+          if (lane == 0) k = atomicAdd(&es.chunk_next, 1);
+          k = __shfl_sync(kFull, k, 0);
+          more = k < n_chunks;
+          if (more) {
+            const int u = k * 32 + lane;
+            // owner triangle of unit u: the owner of the chunk's first unit plus
+            // the triangles starting inside the chunk up to u (all have >= 1 row)
+            const int o0 = s_rowner[k];
+            const int mi = o0 + 1 + lane;
+            uint32_t bit = 0;
+            if (mi < n_round) {
+              const int d = (int)s_span[mi].row0 - k * 32;  // >= 1
+              if (d < 32) bit = 1u << d;
+            }
+            const uint32_t starts = __reduce_or_sync(kFull, bit);
+            const int j = o0 + __popc(starts & lanemask_le);
+            int len = 0, x0 = 0, row = 0;
+            if (u < n_rows) {
+              const SpanRec &S = s_span[j];
+              row = (int)S.py0 + (u - (int)S.row0);
+              len = row_span(S, row, x0);
+            }
+            const uint32_t sm = __ballot_sync(kFull, len > 0);
+            if (len > 0)
+              q[qn + __popc(sm & lanemask_lt)] =
+                  make_uint2((uint32_t)x0 | ((uint32_t)len << 16), (uint32_t)row | ((uint32_t)j << 16));
+            qn += __popc(sm);
+          }
+          while (qn >= 32 || (!more && qn > 0)) {
+            __syncwarp();
+            const int nb = min(qn, 32);
+            qn -= nb;
+            int len = 0, x0 = 0, row = 0, j = 0;
+            if (lane < nb) {
+              const uint2 sp = q[qn + lane];
+              x0 = (int)(sp.x & 0xffffu);
+              len = (int)(sp.x >> 16);
+              row = (int)(sp.y & 0xffffu);
+              j = (int)(sp.y >> 16);
+            }
+            __syncwarp();
+            // expand the 32 spans into pixel candidates
+            const int incl = warp_incl_scan(len, lane);
+            const int excl = incl - len;
+            const int N = __shfl_sync(kFull, incl, 31);
+            for (int c0 = 0; c0 < N; c0 += 32) {
+              // span lane of candidate c = c0 + lane: the number of lanes whose
+              // inclusive end is <= c (branch-free binary search over the scan)
+              const int c = c0 + lane;
+              int owner = 0;
+    #pragma unroll
+              for (int s = 16; s >= 1; s >>= 1) {
+                const int v = __shfl_sync(kFull, incl, owner + s - 1);
+                if (v <= c) owner += s;
+              }
+              const int o_ex = __shfl_sync(kFull, excl, owner & 31);
+              const int o_x0 = __shfl_sync(kFull, x0, owner & 31);
+              const int o_row = __shfl_sync(kFull, row, owner & 31);
+              const int o_tri = __shfl_sync(kFull, j, owner & 31);
+              bool cov = false;
+              uint32_t pix = 0;
+              double z = 0.0;
+              if (c < N) {
+                const int px = o_x0 + (c - o_ex);
+                pix = (uint32_t)((o_row - y0) * p.W + px);
+                cov = eval_exact(s_rec[o_tri], px, o_row, s_vxy64, s_viz, z);
+              }
+              const uint32_t cm = __ballot_sync(kFull, cov);
+              if (cm == 0u) continue;
+              const int leader = __ffs(cm) - 1;
+              int slot = 0;
+              if (lane == leader) slot = atomicAdd(&es.n_frag, __popc(cm));
+              slot = __shfl_sync(kFull, slot, leader) + __popc(cm & lanemask_lt);
+              if (cov) {
+                const float zf = (float)z;
+                const uint32_t zb = __float_as_uint(zf);
+                if (zb < atomicMin(&s_dbits[pix], zb)) atomicOr(&s_wkey[pix], kDecBit);
+                if (slot < p.frag_limit)
+                  s_frag[slot] = make_uint2(zb | (z < (double)zf ? 0x80000000u : 0u),
+                                            pix | ((uint32_t)o_tri << 20));
               }
             }
           }
-          __syncthreads();
         }
-        if (r1 < n_live)
-          for (int i = tid; i < npx; i += kThreads) s_wkey[i] = 0u;
-      }
-      __syncthreads();
-      r0 = r1;
-    }
-    if (warp == kWarps - 1 && !prepared)  // env without live triangles
-      prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es, lane);
+        __syncthreads();
 
-    // ---- phase 5: composite + postprocess (distractor.py:140-176, env.py:168-173)
-    if (p.mode == PXR_MODE_VIDEO && p.vframe_bulk) mbar_wait_parity(&es.vbar, vphase);
-    vphase ^= 1u;
-    const uint8_t *vsrc = p.mode == PXR_MODE_VIDEO
-                              ? (p.vframe_bulk ? s_vframe
-                                               : p.frames + es.frame_idx[cb] * p.vframe_bytes)
-                              : nullptr;
-    // Four consecutive pixels per thread: 12 colour bytes are three aligned
-    // words; the colour bias is a per-byte saturating add/sub (__vaddus4 /
-    // __vsubus4 == clamp(v + b, 0, 255) for |b| <= 255).
-    uint32_t bpos[3] = {0u, 0u, 0u}, bneg[3] = {0u, 0u, 0u};
-    if (p.mode == PXR_MODE_COLOR) {
-      for (int byte = 0; byte < 12; byte++) {
-        const int bc = es.bias[cb][byte % 3];
-        bpos[byte >> 2] |= (uint32_t)(bc > 0 ? bc : 0) << (8 * (byte & 3));
-        bneg[byte >> 2] |= (uint32_t)(bc < 0 ? -bc : 0) << (8 * (byte & 3));
-      }
-    }
-    const bool row_groups = (p.W & 3) == 0;  // a 4-pixel group never wraps a row
-    const int ngroups = npx >> 2;
-    for (int gi = tid; gi < ngroups; gi += kThreads) {
-      const int i0 = gi << 2;
-      const float4 d4 = reinterpret_cast<const float4 *>(s_depth)[gi];
-      const float d[4] = {d4.x, d4.y, d4.z, d4.w};
-      const bool bg[4] = {isinf(d4.x), isinf(d4.y), isinf(d4.z), isinf(d4.w)};
-      uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
-      uint32_t w[3];
-      const bool video = p.mode == PXR_MODE_VIDEO;
-      w[0] = c3[0]; w[1] = c3[1]; w[2] = c3[2];
-      if (plan_ok) {  // branch-free: texel words merged under per-pixel byte masks
-        const int y = (int)__umulhi((uint32_t)i0, p.wmagic);
-        const int x = i0 - y * p.W;
-        const uint4 pl = s_gplan[x >> 2];
-        const uint32_t *src = reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y]) + pl.x;
-        const uint32_t sels[3] = {pl.y, pl.z, pl.w};
-        const uint32_t m[3] = {
-            (bg[0] ? 0x00ffffffu : 0u) | (bg[1] ? 0xff000000u : 0u),
-            (bg[1] ? 0x0000ffffu : 0u) | (bg[2] ? 0xffff0000u : 0u),
-            (bg[2] ? 0x000000ffu : 0u) | (bg[3] ? 0xffffff00u : 0u)};
-#pragma unroll
-        for (int q = 0; q < 3; q++) {
-          const uint32_t *wp = src + (sels[q] >> 16);
-          const uint32_t t = __byte_perm(wp[0], wp[1], sels[q] & 0xffffu);
-          w[q] = (t & m[q]) | (w[q] & ~m[q]);
-        }
-      } else if (video && (bg[0] | bg[1] | bg[2] | bg[3])) {  // distractor.py:172-176
-        int y = (int)__umulhi((uint32_t)i0, p.wmagic);
-        int x = i0 - y * p.W;
-        if (p.vframe_bulk && row_groups) {
-          const uint32_t rb = s_rowmap[y];
-          const uint4 cm = *reinterpret_cast<const uint4 *>(s_colmap + x);
-          const uint32_t cms[4] = {cm.x, cm.y, cm.z, cm.w};
-#pragma unroll
-          for (int k = 0; k < 4; k++) {
-            if (!bg[k]) continue;
-            const uint32_t off = rb + cms[k];  // 24-bit texel from two aligned words
-            const uint32_t *wp = reinterpret_cast<const uint32_t *>(s_vframe + (off & ~3u));
-            put_texel(w, k, __funnelshift_r(wp[0], wp[1], 8 * (off & 3u)) & 0xffffffu);
+        // exact sequential-order resolve (see the file header)
+        const int n_frag = es.n_frag;
+        if (n_frag <= p.frag_limit) {
+          for (int i = tid; i < n_frag; i += kThreads) {
+            const uint2 f = s_frag[i];
+            const uint32_t pix = f.y & 0xFFFFFu, tri = f.y >> 20;
+            if ((f.x & 0x7FFFFFFFu) == s_dbits[pix]) {  // in S: z < F == z < RN32(z)
+              const uint32_t hb = s_wkey[pix] & kDecBit;  // stable after the barrier
+              atomicMax(&s_wkey[pix], hb | ((f.x >> 31) ? 0x10000u + tri : 0xFFFFu - tri));
+            }
+          }
+          __syncthreads();
+          for (int i = tid; i < n_frag; i += kThreads) {
+            const uint32_t pix = s_frag[i].y & 0xFFFFFu, tri = s_frag[i].y >> 20;
+            if (resolve_winner(s_wkey[pix]) == (int)tri) put_rgb(s_col, pix, s_rec[tri].rgb);
+          }
+          if (r1 < n_live) {
+            __syncthreads();
+            for (int i = tid; i < n_frag; i += kThreads) s_wkey[s_frag[i].y & 0xFFFFFu] = 0u;
           }
         } else {
+          // fragment list overflow: recompute the candidates for both passes
+          for (int pass = 0; pass < 2; pass++) {
+            for (int u = tid; u < n_rows; u += kThreads) {
+              int j = s_rowner[u >> 5];
+              while (j + 1 < n_round && s_span[j + 1].row0 <= (uint32_t)u) j++;
+              const SpanRec &S = s_span[j];
+              const TriRec &R = s_rec[j];
+              const int row = (int)S.py0 + (u - (int)S.row0);
+              int x0;
+              const int len = row_span(S, row, x0);
+              for (int px = x0; px < x0 + len; px++) {
+                double z;
+                if (!eval_exact(R, px, row, s_vxy64, s_viz, z)) continue;
+                const uint32_t pix = (uint32_t)((row - y0) * p.W + px);
+                const uint32_t F = s_dbits[pix];
+                if (__float_as_uint((float)z) != F) continue;
+                if (pass == 0) {
+                  const uint32_t hb = s_wkey[pix] & kDecBit;
+                  atomicMax(&s_wkey[pix],
+                            hb | (z < (double)__uint_as_float(F) ? 0x10000u + j : 0xFFFFu - j));
+                } else if (resolve_winner(s_wkey[pix]) == j) {
+                  put_rgb(s_col, pix, R.rgb);
+                }
+              }
+            }
+            __syncthreads();
+          }
+          if (r1 < n_live)
+            for (int i = tid; i < npx; i += kThreads) s_wkey[i] = 0u;
+        }
+        __syncthreads();
+        r0 = r1;
+      }
+      if (warp == kWarps - 1 && !prepared)  // env without live triangles
+        prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es, lane);
+
+      // ---- phase 5: composite + postprocess (distractor.py:140-176, env.py:168-173)
+      if (y0 == 0) {  // the env's video frame (one fetch for all bands)
+        if (p.mode == PXR_MODE_VIDEO && p.vframe_bulk) mbar_wait_parity(&es.vbar, vphase);
+        vphase ^= 1u;
+      }
+      const uint8_t *vsrc = p.mode == PXR_MODE_VIDEO
+                                ? (p.vframe_bulk ? s_vframe
+                                                 : p.frames + es.frame_idx[cb] * p.vframe_bytes)
+                                : nullptr;
+      // Four consecutive pixels per thread: 12 colour bytes are three aligned
+      // words; the colour bias is a per-byte saturating add/sub (__vaddus4 /
+      // __vsubus4 == clamp(v + b, 0, 255) for |b| <= 255).
+      uint32_t bpos[3] = {0u, 0u, 0u}, bneg[3] = {0u, 0u, 0u};
+      if (p.mode == PXR_MODE_COLOR) {
+        for (int byte = 0; byte < 12; byte++) {
+          const int bc = es.bias[cb][byte % 3];
+          bpos[byte >> 2] |= (uint32_t)(bc > 0 ? bc : 0) << (8 * (byte & 3));
+          bneg[byte >> 2] |= (uint32_t)(bc < 0 ? -bc : 0) << (8 * (byte & 3));
+        }
+      }
+      const bool row_groups = (p.W & 3) == 0;  // a 4-pixel group never wraps a row
+      const int ngroups = npx >> 2;
+      for (int gi = tid; gi < ngroups; gi += kThreads) {
+        const int i0 = gi << 2;
+        const float4 d4 = reinterpret_cast<const float4 *>(s_depth)[gi];
+        const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+        const bool bg[4] = {isinf(d4.x), isinf(d4.y), isinf(d4.z), isinf(d4.w)};
+        uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
+        uint32_t w[3];
+        const bool video = p.mode == PXR_MODE_VIDEO;
+        w[0] = c3[0]; w[1] = c3[1]; w[2] = c3[2];
+        if (plan_ok) {  // branch-free: texel words merged under per-pixel byte masks
+          const int y = (int)__umulhi((uint32_t)i0, p.wmagic);
+          const int x = i0 - y * p.W;
+          const uint4 pl = s_gplan[x >> 2];
+          const uint32_t *src =
+              reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y0 + y]) + pl.x;
+          const uint32_t sels[3] = {pl.y, pl.z, pl.w};
+          const uint32_t m[3] = {
+              (bg[0] ? 0x00ffffffu : 0u) | (bg[1] ? 0xff000000u : 0u),
+              (bg[1] ? 0x0000ffffu : 0u) | (bg[2] ? 0xffff0000u : 0u),
+              (bg[2] ? 0x000000ffu : 0u) | (bg[3] ? 0xffffff00u : 0u)};
+#pragma unroll
+          for (int q = 0; q < 3; q++) {
+            const uint32_t *wp = src + (sels[q] >> 16);
+            const uint32_t t = __byte_perm(wp[0], wp[1], sels[q] & 0xffffu);
+            w[q] = (t & m[q]) | (w[q] & ~m[q]);
+          }
+        } else if (video && (bg[0] | bg[1] | bg[2] | bg[3])) {  // distractor.py:172-176
+          int y = (int)__umulhi((uint32_t)i0, p.wmagic);
+          int x = i0 - y * p.W;
+          y += y0;  // frame row
+          if (p.vframe_bulk && row_groups) {
+            const uint32_t rb = s_rowmap[y];
+            const uint4 cm = *reinterpret_cast<const uint4 *>(s_colmap + x);
+            const uint32_t cms[4] = {cm.x, cm.y, cm.z, cm.w};
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              if (!bg[k]) continue;
+              const uint32_t off = rb + cms[k];  // 24-bit texel from two aligned words
+              const uint32_t *wp = reinterpret_cast<const uint32_t *>(s_vframe + (off & ~3u));
+              put_texel(w, k, __funnelshift_r(wp[0], wp[1], 8 * (off & 3u)) & 0xffffffu);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              if (bg[k]) {
+                const uint8_t *src = vsrc + s_rowmap[y] + s_colmap[x];
+                put_texel(w, k, (uint32_t)src[0] | ((uint32_t)src[1] << 8) |
+                                    ((uint32_t)src[2] << 16));
+              }
+              if (++x == p.W) { x = 0; y++; }
+            }
+          }
+        } else if (p.mode == PXR_MODE_COLOR) {  // distractor.py:149-161
+          for (int q = 0; q < 3; q++) w[q] = __vsubus4(__vaddus4(w[q], bpos[q]), bneg[q]);
+        }
+        if (p.gray) {  // env.py:168-173
+          uint32_t gw = 0;
 #pragma unroll
           for (int k = 0; k < 4; k++) {
-            if (bg[k]) {
-              const uint8_t *src = vsrc + s_rowmap[y] + s_colmap[x];
-              put_texel(w, k, (uint32_t)src[0] | ((uint32_t)src[1] << 8) |
-                                  ((uint32_t)src[2] << 16));
+            uint32_t ch3[3];
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++) {
+              const int byte = 3 * k + ch;
+              ch3[ch] = (w[byte >> 2] >> (8 * (byte & 3))) & 0xffu;
             }
-            if (++x == p.W) { x = 0; y++; }
+            gw |= ((299u * ch3[0] + 587u * ch3[1] + 114u * ch3[2] + 500u) / 1000u) << (8 * k);
           }
+          reinterpret_cast<uint32_t *>(s_gray)[gi] = gw;
+        } else {
+          c3[0] = w[0]; c3[1] = w[1]; c3[2] = w[2];
         }
-      } else if (p.mode == PXR_MODE_COLOR) {  // distractor.py:149-161
-        for (int q = 0; q < 3; q++) w[q] = __vsubus4(__vaddus4(w[q], bpos[q]), bneg[q]);
+        if (p.out_depth != nullptr) {
+          float *dd = p.out_depth + (int64_t)env * fpx + (int64_t)y0 * p.W + i0;
+          if (p.depth_vec) *reinterpret_cast<float4 *>(dd) = d4;
+          else for (int k = 0; k < 4; k++) dd[k] = d[k];
+        }
       }
-      if (p.gray) {  // env.py:168-173
-        uint32_t gw = 0;
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-          uint32_t ch3[3];
-#pragma unroll
+      for (int i = (ngroups << 2) + tid; i < npx; i += kThreads) {  // tail pixels
+        const float d = s_depth[i];
+        uint32_t rgb = s_col[3 * i] | (s_col[3 * i + 1] << 8) | (s_col[3 * i + 2] << 16);
+        if (p.mode == PXR_MODE_VIDEO && isinf(d)) {
+          const int y = (int)__umulhi((uint32_t)i, p.wmagic), x = i - y * p.W;
+          const uint8_t *src = vsrc + s_rowmap[y0 + y] + s_colmap[x];
+          rgb = (uint32_t)src[0] | ((uint32_t)src[1] << 8) | ((uint32_t)src[2] << 16);
+        } else if (p.mode == PXR_MODE_COLOR) {
+          uint32_t o = 0;
           for (int ch = 0; ch < 3; ch++) {
-            const int byte = 3 * k + ch;
-            ch3[ch] = (w[byte >> 2] >> (8 * (byte & 3))) & 0xffu;
+            const int v = (int)((rgb >> (8 * ch)) & 0xffu) + es.bias[cb][ch];
+            o |= (uint32_t)min(255, max(0, v)) << (8 * ch);
           }
-          gw |= ((299u * ch3[0] + 587u * ch3[1] + 114u * ch3[2] + 500u) / 1000u) << (8 * k);
+          rgb = o;
         }
-        reinterpret_cast<uint32_t *>(s_gray)[gi] = gw;
-      } else {
-        c3[0] = w[0]; c3[1] = w[1]; c3[2] = w[2];
-      }
-      if (p.out_depth != nullptr) {
-        float *dd = p.out_depth + (int64_t)env * npx + i0;
-        if (p.depth_vec) *reinterpret_cast<float4 *>(dd) = d4;
-        else for (int k = 0; k < 4; k++) dd[k] = d[k];
-      }
-    }
-    for (int i = (ngroups << 2) + tid; i < npx; i += kThreads) {  // tail pixels
-      const float d = s_depth[i];
-      uint32_t rgb = s_col[3 * i] | (s_col[3 * i + 1] << 8) | (s_col[3 * i + 2] << 16);
-      if (p.mode == PXR_MODE_VIDEO && isinf(d)) {
-        const int y = (int)__umulhi((uint32_t)i, p.wmagic), x = i - y * p.W;
-        const uint8_t *src = vsrc + s_rowmap[y] + s_colmap[x];
-        rgb = (uint32_t)src[0] | ((uint32_t)src[1] << 8) | ((uint32_t)src[2] << 16);
-      } else if (p.mode == PXR_MODE_COLOR) {
-        uint32_t o = 0;
-        for (int ch = 0; ch < 3; ch++) {
-          const int v = (int)((rgb >> (8 * ch)) & 0xffu) + es.bias[cb][ch];
-          o |= (uint32_t)min(255, max(0, v)) << (8 * ch);
+        if (p.gray) {
+          s_gray[i] = (uint8_t)((299u * (rgb & 0xffu) + 587u * ((rgb >> 8) & 0xffu) +
+                                 114u * ((rgb >> 16) & 0xffu) + 500u) / 1000u);
+        } else {
+          put_rgb(s_col, (uint32_t)i, rgb);
         }
-        rgb = o;
+        if (p.out_depth != nullptr) p.out_depth[(int64_t)env * fpx + (int64_t)y0 * p.W + i] = d;
       }
-      if (p.gray) {
-        s_gray[i] = (uint8_t)((299u * (rgb & 0xffu) + 587u * ((rgb >> 8) & 0xffu) +
-                               114u * ((rgb >> 16) & 0xffu) + 500u) / 1000u);
-      } else {
-        put_rgb(s_col, (uint32_t)i, rgb);
-      }
-      if (p.out_depth != nullptr) p.out_depth[(int64_t)env * npx + i] = d;
-    }
 
-    // ---- phase 6: frame -> HBM (one TMA bulk store) --------------------
-    uint8_t *gout = p.out + (int64_t)env * p.frame_bytes;
-    if (p.use_bulk) {
-      fence_proxy_async_smem();
-      __syncthreads();
-      if (tid == 0) bulk_store_s2g(gout, s_out, (uint32_t)p.frame_bytes);
-    } else {
-      __syncthreads();
-      for (int i = tid; i < p.frame_bytes; i += kThreads) gout[i] = s_out[i];
-      __syncthreads();
-    }
+      // ---- phase 6: frame -> HBM (one TMA bulk store) --------------------
+      uint8_t *gout = p.out + (int64_t)env * p.frame_bytes + (int64_t)y0 * p.W * chans;
+      const int band_bytes = npx * chans;
+      if (p.use_bulk) {  // host: every band's size and offset are multiples of 16
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) bulk_store_s2g(gout, s_out, (uint32_t)band_bytes);
+      } else {
+        __syncthreads();
+        for (int i = tid; i < band_bytes; i += kThreads) gout[i] = s_out[i];
+        __syncthreads();
+      }
+      yb += band_h;
+    } while (kBands && yb < p.H);
   }
   if (tid == 0 && p.use_bulk) bulk_wait_all();
 }
@@ -1302,6 +1331,8 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     if (v > 0) p.row_cap = v > p.H ? v : p.H;
   }
   if (const char *s = getenv("PXR_DEBUG_CAP")) debug_cap = atoi(s);
+  int debug_band = 0;
+  if (const char *s = getenv("PXR_DEBUG_BAND_H")) debug_band = atoi(s);
 
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1313,6 +1344,27 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   // largest count that does (extra rounds handle the rest exactly).
   int cap = p.nt > 0 ? (p.nt < kMaxCap ? p.nt : kMaxCap) : 1;
   if (debug_cap > 0 && debug_cap < cap) cap = debug_cap;
+  // Bands: the whole frame when its per-pixel state fits next to a useful
+  // record capacity, else the tallest band that does; full bands are whole
+  // multiples of 16 bytes so every band's TMA store stays legal.
+  {
+    const int min_cap = cap < 256 ? cap : 256;
+    const int bytes_row = width * C;
+    int m = 1;  // rows per 16-byte multiple
+    while ((m * bytes_row) % 16 != 0 && m < 16) m *= 2;
+    int bh = height;
+    for (int nb = 1; nb <= height; nb++) {
+      bh = (height + nb - 1) / nb;
+      if (nb > 1 && bh > m) bh -= bh % m;
+      p.band_h = bh;
+      p.cap = min_cap;
+      if (smem_layout(p).total <= budget) break;
+    }
+    if (debug_band > 0 && debug_band < bh) bh = debug_band;
+    p.band_h = bh;
+    if (bh < height && (bh * bytes_row) % 16 != 0) p.use_bulk = 0;
+    if (bh < height && (bh * width) % 4 != 0) p.depth_vec = 0;
+  }
   for (;;) {
     p.cap = cap;
     if (smem_layout(p).total <= budget || cap <= 16) break;
@@ -1320,16 +1372,17 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   }
   const int smem = smem_layout(p).total;
   if (smem > budget) return set_unsupported("frame too large for one CTA's shared memory");
-  cudaError_t e = cudaFuncSetAttribute(render_step_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const bool banded = p.band_h < p.H;
+  auto kernel = banded ? render_step_kernel<true> : render_step_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_step_kernel, kThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
   if (e != cudaSuccess) return set_cuda(e, "occupancy query");
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)num_sms() * per_sm;
   if (grid > batch) grid = batch;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  render_step_kernel<<<(unsigned)grid, kThreads, smem, st>>>(p);
+  kernel<<<(unsigned)grid, kThreads, smem, st>>>(p);
   return check_launch("render_step_kernel");
 }

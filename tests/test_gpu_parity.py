@@ -124,6 +124,8 @@ class TestRenderGolden:
         {"PXR_DEBUG_ROW_CAP": "90"},                   # many bbox-row rounds
         {"PXR_DEBUG_FRAG_LIMIT": "16"},                # fragment-list overflow path
         {"PXR_DEBUG_CAP": "24", "PXR_DEBUG_FRAG_LIMIT": "0"},
+        {"PXR_DEBUG_BAND_H": "20"},                    # row bands (TMA store per band)
+        {"PXR_DEBUG_BAND_H": "7", "PXR_DEBUG_CAP": "40"},  # bands + rounds, plain stores
     ])
     def test_round_and_overflow_paths_exact(self, torch, pkg, monkeypatch, knobs):
         """The multi-round and fragment-overflow paths (only reached by large
@@ -146,7 +148,8 @@ class TestRenderGolden:
                                     84, 84, False)
         np.testing.assert_array_equal(fr.pixels.cpu().numpy(), rec["pixels_fib0"])
 
-    @pytest.mark.parametrize("hw", [(8, 8), (17, 33), (96, 80), (130, 90)])
+    @pytest.mark.parametrize("hw", [(8, 8), (17, 33), (96, 80), (130, 90), (256, 256),
+                                    (200, 152)])
     def test_odd_sizes_vs_oracle(self, torch, pkg, oracle, hw):
         H, W = hw
         rec = golden("render_walker_lite.npz")
@@ -299,6 +302,15 @@ def fused_replay(torch, pkg, tag):
 
 @pytest.mark.parametrize("tag", REPLAYS)
 def test_fused_replay_hash_chain(torch, pkg, tag):
+    fused_replay(torch, pkg, tag)
+
+
+@pytest.mark.parametrize("tag,band", [("walker_video_b8", "12"), ("hopper_color_gray_b4", "5"),
+                                      ("humanoid_video_b8_slice", "32")])
+def test_fused_replay_hash_chain_banded(torch, pkg, monkeypatch, tag, band):
+    """The same chains with the frame forced into row bands (the path large
+    frames take): per-band raster, composite, grayscale and store."""
+    monkeypatch.setenv("PXR_DEBUG_BAND_H", band)
     fused_replay(torch, pkg, tag)
 
 
