@@ -3,7 +3,8 @@
 Mirrors ``pixelctrl.render`` (/root/reference/pkg/src/pixelctrl/render.py):
 constants (50-68), ``Mesh``/``Pose``/``Camera``/``CameraConfig``/``Frame``
 (71-130), tessellation (137-230), the tracking camera (237-279),
-``RobotGeometry`` (559-591) and ``render_robot_batch`` (594-623).
+``RobotGeometry`` (559-591), ``render_robot_batch`` (594-623) and the generic
+scene API ``render`` / ``render_batch`` (491-552) on the same raster kernel.
 
 What changes is where the work runs: tessellation and the camera block are
 host-side and one-time (as in the reference); every per-step array --
@@ -27,7 +28,7 @@ __all__ = [
     "SKY_COLOR", "FLOOR_LIGHT", "FLOOR_DARK", "AMBIENT", "DIFFUSE", "LIGHT_DIR",
     "LINK_PALETTE", "Mesh", "Pose", "Camera", "CameraConfig", "Frame",
     "tessellate_capsule", "tessellate_sphere", "track_camera", "camera_basis",
-    "RobotGeometry", "RobotRenderer", "render_robot_batch",
+    "RobotGeometry", "RobotRenderer", "render_robot_batch", "render", "render_batch",
 ]
 
 SKY_COLOR = (135, 206, 235)
@@ -386,3 +387,100 @@ def render_robot_batch(geom: RobotGeometry, poses, cam_config: CameraConfig, wid
     r.render(poses, floor_in_background=floor_in_background, out_obs=out.pixels,
              out_depth=out.depth)
     return out
+
+
+# ---------------------------------------------------------------- scenes
+
+
+def _scene_world(meshes):
+    """World-space vertices, triangles and per-triangle colours of a scene,
+    with the reference's arithmetic (render.py:504-522): Python f64 cos/sin
+    of the pitch rounded to f32, then f32 ``(x + vx c) - vz s``,
+    ``y + vy``, ``(z + vx s) + vz c``; triangle indices offset per mesh in
+    list order (the z-buffer tie-break order)."""
+    verts, tris, cols = [], [], []
+    base = 0
+    for mesh, pose in meshes:
+        v = np.asarray(mesh.vertices, dtype=np.float32)
+        cf, sf = np.float32(math.cos(pose.pitch)), np.float32(math.sin(pose.pitch))
+        w = np.empty_like(v)
+        w[:, 0] = (np.float32(pose.x) + v[:, 0] * cf) - v[:, 2] * sf
+        w[:, 1] = np.float32(pose.y) + v[:, 1]
+        w[:, 2] = (np.float32(pose.z) + v[:, 0] * sf) + v[:, 2] * cf
+        t = np.asarray(mesh.triangles, dtype=np.int32)
+        verts.append(w)
+        tris.append(t + np.int32(base))
+        cols.append(np.broadcast_to(np.asarray(mesh.base_color, dtype=np.float32), (len(t), 3)))
+        base += len(v)
+    if not verts:
+        return (np.zeros((0, 3), np.float32), np.zeros((0, 3), np.int32),
+                np.zeros((0, 3), np.float32))
+    return (np.ascontiguousarray(np.concatenate(verts)), np.ascontiguousarray(np.concatenate(tris)),
+            np.ascontiguousarray(np.concatenate(cols)))
+
+
+def _render_scene_into(meshes, camera: Camera, light_dir, width: int, height: int,
+                       floor_in_background: bool, pixels, depth, device) -> None:
+    """One scene through pxr_render_step: the world-space mesh is a one-link
+    geometry at the identity pose, the camera block is ``camera_basis`` and
+    the per-env camera position is the block's eye."""
+    import torch
+
+    blk_np = camera_basis(camera)
+    verts, tris, cols = _scene_world(meshes)
+    if len(verts) > 65535 or len(tris) > 65535:
+        raise ValueError("scene too large for the raster kernel (max 65535 vertices / triangles)")
+    t = {
+        "v": torch.from_numpy(verts).to(device),
+        "l": torch.zeros(len(verts), dtype=torch.int32, device=device),
+        "t": torch.from_numpy(tris).to(device),
+        "c": torch.from_numpy(cols).to(device),
+        "pose": torch.zeros((1, 1, 3), dtype=torch.float64, device=device),
+        "rays": torch.empty((height, width, 3), dtype=torch.float64, device=device),
+    }
+    geom_c = _native.Geometry(t["v"].data_ptr(), t["l"].data_ptr(), t["t"].data_ptr(),
+                              t["c"].data_ptr(), len(verts), len(tris), 1)
+    blk = (ctypes.c_float * 15)(*blk_np.tolist())
+    sep = ctypes.c_int32(0)
+    st = _native.stream_ptr()
+    _native.check(_native.lib().pxr_floor_rays(blk, height, width, t["rays"].data_ptr(),
+                                               ctypes.byref(sep), st))
+    light = np.asarray(light_dir, dtype=np.float32)
+    cam_c = _native.Camera(blk, float(blk_np[0]), float(blk_np[2]),
+                           (ctypes.c_float * 3)(*light.tolist()), t["rays"].data_ptr(),
+                           int(sep.value))
+    dist_c = _native.Distractor(_native.MODE_NONE)
+    _native.check(_native.lib().pxr_render_step(
+        ctypes.byref(geom_c), ctypes.byref(cam_c), t["pose"].data_ptr(), 1, height, width,
+        int(not floor_in_background), ctypes.byref(dist_c), None, 0, None, None, 0,
+        pixels.data_ptr(), depth.data_ptr(), st))
+
+
+def render(meshes, camera: Camera, light_dir=LIGHT_DIR, width: int = 84, height: int = 84,
+           floor_in_background: bool = False) -> Frame:
+    """render.py:491-533 on the B200: one scene of posed meshes, a batch-1
+    ``Frame`` of CUDA tensors, bit-identical to the reference."""
+    if width < 8 or height < 8:
+        raise ValueError("render needs width, height >= 8")
+    dev = _native.require_cuda()
+    frame = Frame.allocate(1, int(height), int(width), device=dev)
+    _render_scene_into(list(meshes), camera, light_dir, int(width), int(height),
+                       floor_in_background, frame.pixels, frame.depth, dev)
+    return frame
+
+
+def render_batch(scenes, width: int = 84, height: int = 84, floor_in_background: bool = False,
+                 light_dir=LIGHT_DIR) -> Frame:
+    """render.py:536-552: independent scenes, scene i bit-identical to
+    ``render(scene i)``; one launch per scene into its slice of the batch."""
+    scenes = list(scenes)
+    if not scenes:
+        raise ValueError("render_batch needs at least one scene")
+    if width < 8 or height < 8:
+        raise ValueError("render needs width, height >= 8")
+    dev = _native.require_cuda()
+    frame = Frame.allocate(len(scenes), int(height), int(width), device=dev)
+    for i, (meshes, camera) in enumerate(scenes):
+        _render_scene_into(list(meshes), camera, light_dir, int(width), int(height),
+                           floor_in_background, frame.pixels[i:i + 1], frame.depth[i:i + 1], dev)
+    return frame

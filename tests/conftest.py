@@ -64,3 +64,19 @@ def oracle():
 
     O.build()
     return O
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as _t
+
+    return _t
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    """The package with its CUDA library loaded (GPU tests)."""
+    import paper_2502_00021_b200 as P
+
+    P._native.lib()
+    return P

@@ -31,7 +31,9 @@ from pixelctrl.models import builtin_model, load_model  # noqa: E402
 from pixelctrl.physics import forward_kinematics, model_arrays  # noqa: E402
 from pixelctrl.prng import fold_in, key_from_seed  # noqa: E402
 from pixelctrl.recorder import make_policy  # noqa: E402
-from pixelctrl.render import CameraConfig, Frame, RobotGeometry, render_robot_batch  # noqa: E402
+from pixelctrl.render import (  # noqa: E402
+    LINK_PALETTE, Camera, CameraConfig, Frame, Mesh, Pose, RobotGeometry, render, render_batch,
+    render_robot_batch, tessellate_capsule, tessellate_sphere)
 from pixelctrl.video_pack import VideoPack, save_video_pack  # noqa: E402
 from pixelctrl.video_tools import generate_synthetic_pack  # noqa: E402
 
@@ -234,14 +236,102 @@ def physics_fixture():
     np.savez_compressed(os.path.join(HERE, "physics.npz"), **rec)
 
 
+def _scene_list():
+    """Deterministic scenes for the generic render()/render_batch() API
+    (render.py:491-552): random two-triangle scenes in the style of the
+    reference's ray-cast acceptance test (tests/test_acceptance.py:158-188),
+    posed sphere/capsule scenes under general cameras with and without the
+    floor, and the 256x256 sphere of the silhouette test (190-199)."""
+    rng = np.random.default_rng(7)
+    scenes = []
+    cam0 = Camera(eye=(0.0, -3.0, 0.5), target=(0.0, 1.0, 0.5))
+    for _ in range(40):
+        v = np.empty((6, 3), dtype=np.float32)
+        v[:, 0] = rng.uniform(-2.0, 2.0, 6)
+        v[:, 1] = rng.uniform(1.5, 6.0, 6)
+        v[:, 2] = rng.uniform(-1.5, 3.0, 6)
+        meshes = [(Mesh(v[3 * i:3 * i + 3].copy(), np.array([[0, 1, 2]], dtype=np.int32),
+                        tuple(LINK_PALETTE[int(rng.integers(len(LINK_PALETTE)))])), Pose())
+                  for i in range(2)]
+        scenes.append((meshes, cam0, 32, 32, True))
+    for k in range(12):
+        meshes = []
+        for j in range(int(rng.integers(1, 4))):
+            if rng.random() < 0.5:
+                m = tessellate_sphere(float(rng.uniform(0.2, 0.8)), int(rng.integers(3, 12)),
+                                      int(rng.integers(4, 16)))
+            else:
+                m = tessellate_capsule(float(rng.uniform(0.05, 0.3)), float(rng.uniform(0.2, 1.2)),
+                                       int(rng.integers(2, 6)), int(rng.integers(3, 12)),
+                                       LINK_PALETTE[j % len(LINK_PALETTE)])
+            pose = Pose(x=float(rng.uniform(-1, 1)), y=float(rng.uniform(-0.5, 0.5)),
+                        z=float(rng.uniform(0.2, 1.5)), pitch=float(rng.uniform(-3, 3)))
+            meshes.append((m, pose))
+        eye = (float(rng.uniform(-2, 2)), float(rng.uniform(-5, -2)), float(rng.uniform(0.5, 3)))
+        cam = Camera(eye=eye, target=(0.0, 0.0, 0.6), vertical_fov=float(rng.uniform(0.5, 1.2)))
+        H, W = [(48, 64), (40, 40), (33, 57)][k % 3]
+        scenes.append((meshes, cam, W, H, bool(k % 2)))
+    sphere = tessellate_sphere(0.8, 32, 48)
+    scenes.append(([(sphere, Pose(z=1.0))], Camera(eye=(0.0, -5.0, 1.0), target=(0.0, 0.0, 1.0)),
+                   256, 256, True))
+    scenes.append(([], cam0, 24, 16, False))  # empty scene: sky + floor only
+    return scenes
+
+
+def scene_fixture():
+    rec = {"mesh_counts": [], "vert_counts": [], "tri_counts": [], "verts": [], "tris": [],
+           "colors": [], "poses": [], "cams": [], "sizes": [], "fib": []}
+    out_px, out_dp = [], []
+    for meshes, cam, W, H, fib in _scene_list():
+        rec["mesh_counts"].append(len(meshes))
+        for m, pose in meshes:
+            rec["vert_counts"].append(len(m.vertices))
+            rec["tri_counts"].append(len(m.triangles))
+            rec["verts"].append(np.asarray(m.vertices, np.float32))
+            rec["tris"].append(np.asarray(m.triangles, np.int32))
+            rec["colors"].append(np.asarray(m.base_color, np.float64))
+            rec["poses"].append([pose.x, pose.y, pose.z, pose.pitch])
+        rec["cams"].append(list(cam.eye) + list(cam.target) + list(cam.up) +
+                           [cam.vertical_fov, cam.near, cam.far])
+        rec["sizes"].append([H, W])
+        rec["fib"].append(fib)
+        fr = render(meshes, cam, width=W, height=H, floor_in_background=fib)
+        out_px.append(fr.pixels[0].reshape(-1))
+        out_dp.append(fr.depth[0].reshape(-1))
+    arrs = {
+        "mesh_counts": np.array(rec["mesh_counts"], np.int64),
+        "vert_counts": np.array(rec["vert_counts"], np.int64),
+        "tri_counts": np.array(rec["tri_counts"], np.int64),
+        "verts": np.concatenate(rec["verts"]) if rec["verts"] else np.zeros((0, 3), np.float32),
+        "tris": np.concatenate(rec["tris"]) if rec["tris"] else np.zeros((0, 3), np.int32),
+        "colors": np.array(rec["colors"], np.float64),
+        "poses": np.array(rec["poses"], np.float64),
+        "cams": np.array(rec["cams"], np.float64),
+        "sizes": np.array(rec["sizes"], np.int64),
+        "fib": np.array(rec["fib"], bool),
+        "pixels": np.concatenate(out_px),
+        "depth": np.concatenate(out_dp),
+    }
+    # render_batch of three same-size scenes equals the singles (render.py:536-552)
+    sc = [(m, c) for m, c, W, H, fib in _scene_list()[40:52] if (H, W) == (48, 64)][:3]
+    fb = render_batch(sc, width=64, height=48, floor_in_background=False)
+    arrs["batch_pixels"] = fb.pixels
+    arrs["batch_depth"] = fb.depth
+    np.savez_compressed(os.path.join(HERE, "scenes.npz"), **arrs)
+
+
 def main():
     if len(sys.argv) > 1 and sys.argv[1] == "physics":
         physics_fixture()
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "scenes":
+        scene_fixture()
         return
     geometry_fixture()
     render_fixtures()
     distractor_fixtures()
     physics_fixture()
+    scene_fixture()
     pack = os.path.join("/tmp", "golden_replay.pxvp")
     small_pack(pack, seed=21, videos=4, frames=7, size=32)
     # BASELINE config 1: HalfCheetah, 1 env, 84x84, no distractors, 1000 steps.

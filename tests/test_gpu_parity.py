@@ -24,21 +24,6 @@ PIXEL_TOL_LSB = 1
 PIXEL_TOL_FRAC = 0.999
 
 
-@pytest.fixture(scope="module")
-def torch():
-    import torch as _t
-
-    return _t
-
-
-@pytest.fixture(scope="module")
-def pkg():
-    import paper_2502_00021_b200 as P
-
-    P._native.lib()
-    return P
-
-
 def to_dev(torch, a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 

@@ -18,8 +18,9 @@ ap.add_argument("--mode", default="video")
 ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--timed", type=int, default=20)
 ap.add_argument("--grayscale", action="store_true")
+ap.add_argument("--size", type=int, nargs=2, default=(84, 84), metavar=("H", "W"))
 a = ap.parse_args()
-w = Workload(a.model, a.envs, a.mode, grayscale=a.grayscale)
+w = Workload(a.model, a.envs, a.mode, grayscale=a.grayscale, height=a.size[0], width=a.size[1])
 poses = [w.poses(t).clone() for t in range(2)]
 torch.cuda.synchronize()
 for t in range(a.steps):
@@ -31,4 +32,4 @@ for t in range(a.timed):
 ev[1].record()
 torch.cuda.synchronize()
 ms = ev[0].elapsed_time(ev[1]) / max(1, a.timed)
-print(f"{a.model} {a.mode} B={a.envs}: {ms:.3f} ms/launch  {a.envs / ms / 1e3:.2f} M env-steps/s")
+print(f"{a.model} {a.mode} {a.size[0]}x{a.size[1]} B={a.envs}: {ms:.3f} ms/launch  {a.envs / ms / 1e3:.2f} M env-steps/s")
