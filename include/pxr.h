@@ -225,6 +225,17 @@ pxr_status pxr_forward_kinematics(const double *qpos, const int32_t *parent,
                                   const double *anchor_dist, int32_t n_links,
                                   int64_t batch, double *poses, void *stream);
 
+/* Conv-stub policy forward (bench.py:36-145 ConvStub / conv_stub_forward /
+ * _conv_forward_range): obs u8 (B, H, W, C) -> actions f64 (B, J) =
+ * tanh(relu(conv16x8x8s4(obs * f32(1/255))) @ proj), f32 arithmetic.
+ * conv: f32 (8*8*C, 16), row (ky, kx, c); proj: f32 (oh*ow*16, J), feature
+ * order (oy, ox, f). Each batch row is computed independently of the batch
+ * (bench.py:131-145 contract). J <= 32. */
+pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, int32_t height,
+                                 int32_t width, int32_t channels, const float *conv,
+                                 const float *proj, int32_t n_joints, double *out,
+                                 void *stream);
+
 #ifdef __cplusplus
 }
 #endif

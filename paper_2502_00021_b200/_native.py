@@ -31,7 +31,7 @@ EXPORTED = (
     "pxr_render_step", "pxr_advance_distractors", "pxr_init_distractors",
     "pxr_apply_color", "pxr_apply_video", "pxr_grayscale", "pxr_threefry2x64",
     "pxr_sincosf", "pxr_pose_source", "pxr_forward_kinematics", "pxr_div_check",
-    "pxr_physics_step", "pxr_reset_envs", "pxr_env_poses",
+    "pxr_physics_step", "pxr_reset_envs", "pxr_env_poses", "pxr_conv_stub_forward",
 )
 
 _vp = ctypes.c_void_p
@@ -144,6 +144,8 @@ def lib() -> ctypes.CDLL:
     L.pxr_pose_source.argtypes = [_vp, _vp, _vp, _i32, _u64, _u64, _u64, _i64, _i64, _vp, _vp]
     L.pxr_forward_kinematics.restype = _i32
     L.pxr_forward_kinematics.argtypes = [_vp, _vp, _vp, _i32, _i64, _vp, _vp]
+    L.pxr_conv_stub_forward.restype = _i32
+    L.pxr_conv_stub_forward.argtypes = [_vp, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _vp]
     L.pxr_physics_step.restype = _i32
     L.pxr_physics_step.argtypes = [P(Model), _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]
     L.pxr_reset_envs.restype = _i32

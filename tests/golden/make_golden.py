@@ -320,7 +320,32 @@ def scene_fixture():
     np.savez_compressed(os.path.join(HERE, "scenes.npz"), **arrs)
 
 
+def policy_fixture():
+    """Conv-stub weights (a pure function of the seed) and the reference's
+    own forward outputs (bench.py:36-145) for three shapes."""
+    from pixelctrl.bench import ConvStub, conv_stub_forward
+
+    rec = {}
+    for tag, (h, w, c, j, seed, b) in {"a": (24, 28, 3, 5, 1, 3), "g": (16, 16, 1, 3, 2, 2),
+                                       "f": (84, 84, 3, 17, 0, 4)}.items():
+        stub = ConvStub.create(h, w, c, j, seed=seed)
+        obs = np.random.default_rng(seed + 100).integers(0, 256, (b, h, w, c), dtype=np.uint8)
+        rec[f"{tag}_shape"] = np.array([h, w, c, j, seed], np.int64)
+        if tag == "f":  # large: only digests of the weights
+            rec["f_weights_sha"] = np.array([sha(stub.conv), sha(stub.conv_blocks), sha(stub.proj)])
+        else:
+            rec[f"{tag}_conv"] = stub.conv
+            rec[f"{tag}_conv_blocks"] = stub.conv_blocks
+            rec[f"{tag}_proj"] = stub.proj
+        rec[f"{tag}_obs"] = obs
+        rec[f"{tag}_actions"] = conv_stub_forward(stub, obs)
+    np.savez_compressed(os.path.join(HERE, "policy.npz"), **rec)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "policy":
+        policy_fixture()
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "physics":
         physics_fixture()
         return
@@ -332,6 +357,7 @@ def main():
     distractor_fixtures()
     physics_fixture()
     scene_fixture()
+    policy_fixture()
     pack = os.path.join("/tmp", "golden_replay.pxvp")
     small_pack(pack, seed=21, videos=4, frames=7, size=32)
     # BASELINE config 1: HalfCheetah, 1 env, 84x84, no distractors, 1000 steps.
