@@ -342,7 +342,38 @@ def policy_fixture():
     np.savez_compressed(os.path.join(HERE, "policy.npz"), **rec)
 
 
+def recorder_fixture():
+    """recorder.py: random-policy actions (a sliced batch), PNG bytes and
+    a PXTJ digest file of a short rollout, all from the reference."""
+    import tempfile
+
+    from pixelctrl import recorder as R
+
+    rec = {}
+    cfg = EnvConfig(model="hopper_lite", batch=5, seed=2, env_offset=3, logical_batch=16)
+    env, _, _ = make_env(cfg)
+    for t in (0, 7):
+        rec[f"random_actions_t{t}"] = R._random_actions(key_from_seed(5), t, env)
+    img = np.random.default_rng(3).integers(0, 256, (13, 17, 3), dtype=np.uint8)
+    rec["png_image"] = img
+    with tempfile.TemporaryDirectory() as d:
+        for tag, im in (("rgb", img), ("gray", img[..., 0])):
+            path = os.path.join(d, f"{tag}.png")
+            R.write_png(im, path)
+            with open(path, "rb") as f:
+                rec[f"png_{tag}_bytes"] = np.frombuffer(f.read(), dtype=np.uint8)
+        dg = R.record_rollout(EnvConfig(model="hopper_lite", batch=2, seed=1), "zeros", 3)
+        path = os.path.join(d, "d.pxtj")
+        R.save_digest(dg, path)
+        with open(path, "rb") as f:
+            rec["digest_file"] = np.frombuffer(f.read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "recorder.npz"), **rec)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "recorder":
+        recorder_fixture()
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "policy":
         policy_fixture()
         return
@@ -358,6 +389,7 @@ def main():
     physics_fixture()
     scene_fixture()
     policy_fixture()
+    recorder_fixture()
     pack = os.path.join("/tmp", "golden_replay.pxvp")
     small_pack(pack, seed=21, videos=4, frames=7, size=32)
     # BASELINE config 1: HalfCheetah, 1 env, 84x84, no distractors, 1000 steps.
