@@ -374,7 +374,9 @@ __device__ __forceinline__ void span_setup(const float2 a, const float2 b, const
     const float2 s = v[k], t = v[(k + 1) % 3];
     const float A = t.x - s.x, B = t.y - s.y;
     if (B != 0.0f) {
-      const float r = A / B;
+      // the slope only feeds a conservative bound: __fdividef's <= 2 ulp
+      // error moves the line by <= 2^-22 |r| (H + |s.y|), far inside m
+      const float r = __fdividef(A, B);
       S.r[k] = r;
       S.c0[k] = __fmaf_rn(-r, s.y, s.x);
       S.m[k] = 0x1p-10f + (fabsf(s.x) + fabsf(r) * (fabsf(s.y) + ymax)) * 0x1p-17f;
@@ -471,7 +473,7 @@ render_step_kernel(const RenderParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ EnvShared es;
   __shared__ DistSlot s_dist[32];
-  __shared__ int s_scan[kWarps];
+  __shared__ int s_scan[2 * kWarps];
   const SmemLayout L = smem_layout(p);
   float4 *s_link = reinterpret_cast<float4 *>(smem + L.link);
   double *s_floor = reinterpret_cast<double *>(smem + L.floor);  // dx[W], dy[H], dz[H]
@@ -653,7 +655,12 @@ render_step_kernel(const RenderParams p) {
       }
 
       // ---- phase 2: liveness (render.py:366-416) + background -------------
-      for (int t = tid; t < p.nt; t += kThreads) {
+      // each thread owns a contiguous block of triangles (index order), so
+      // its live count and bbox-row total feed the block scan directly
+      const int per = (p.nt + kThreads - 1) / kThreads;
+      const int t0 = min(tid * per, p.nt), t1 = min(t0 + per, p.nt);
+      int my_live = 0, my_rows = 0;
+      for (int t = t0; t < t1; t++) {
         uint32_t rows = 0;
         const int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
                   i2 = __ldg(p.tris + 3 * t + 2);
@@ -675,6 +682,8 @@ render_step_kernel(const RenderParams p) {
           }
         }
         s_rows[t] = (uint16_t)rows;
+        my_live += rows != 0u;
+        my_rows += (int)rows;
       }
       // background: sky / floor under an empty z-buffer (render.py:306-344)
       if (p.mode == PXR_MODE_VIDEO && !p.draw_floor) {
@@ -713,31 +722,28 @@ render_step_kernel(const RenderParams p) {
           s_wkey[i] = 0u;
         }
       }
-      __syncthreads();
       // block scan over triangles in index order: live ids, bbox-row prefix
       {
-        const int per = (p.nt + kThreads - 1) / kThreads;
-        const int t0 = min(tid * per, p.nt), t1 = min(t0 + per, p.nt);
-        int nlive = 0, nrows = 0;
-        for (int t = t0; t < t1; t++) {
-          const int r = s_rows[t];
-          nlive += r != 0;
-          nrows += r;
+        const int wl = warp_incl_scan(my_live, lane);
+        const int wr = warp_incl_scan(my_rows, lane);
+        if (lane == 31) {
+          s_scan[warp] = wl;
+          s_scan[kWarps + warp] = wr;
         }
-        const int packed = nlive | (nrows << 12);  // per <= 128 < 2^12 live
-        const int wincl = warp_incl_scan(packed, lane);
-        if (lane == 31) s_scan[warp] = wincl;
-        __syncthreads();
+        __syncthreads();  // (also publishes s_rows and the background)
         if (warp == 0) {
           const int v = lane < kWarps ? s_scan[lane] : 0;
-          const int vi = warp_incl_scan(v, lane);
-          if (lane < kWarps) s_scan[lane] = vi - v;
-          if (lane == kWarps - 1) es.n_live = vi & 0xfff;
+          const int u = lane < kWarps ? s_scan[kWarps + lane] : 0;
+          const int vi = warp_incl_scan(v, lane), ui = warp_incl_scan(u, lane);
+          if (lane < kWarps) {
+            s_scan[lane] = vi - v;
+            s_scan[kWarps + lane] = ui - u;
+          }
+          if (lane == kWarps - 1) es.n_live = vi;
         }
         __syncthreads();
-        const int base = s_scan[warp] + wincl - packed;
-        int li = base & 0xfff;
-        uint32_t racc = (uint32_t)base >> 12;
+        int li = s_scan[warp] + wl - my_live;
+        uint32_t racc = (uint32_t)(s_scan[kWarps + warp] + wr - my_rows);
         for (int t = t0; t < t1; t++) {
           const int r = s_rows[t];
           if (r != 0) {
@@ -1339,7 +1345,7 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   int max_optin = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const int budget =
-      max_optin - (int)(sizeof(EnvShared) + sizeof(DistSlot) * 32 + 4 * kWarps) - 256;
+      max_optin - (int)(sizeof(EnvShared) + sizeof(DistSlot) * 32 + 8 * kWarps) - 256;
   // Live-triangle records per round: all triangles if they fit, else the
   // largest count that does (extra rounds handle the rest exactly).
   int cap = p.nt > 0 ? (p.nt < kMaxCap ? p.nt : kMaxCap) : 1;
