@@ -191,6 +191,7 @@ struct EnvShared {
   int round_end;
   int chunk_next;
   int n_frag;
+  int one_round;  // all live triangles of the band fit one raster round
   int plan_ok;
 };
 
@@ -753,32 +754,46 @@ render_step_kernel(const RenderParams p) {
             racc += (uint32_t)r;
           }
         }
-        if (tid == kThreads - 1) s_lrp[li] = racc;  // the last thread holds the totals
+        if (tid == kThreads - 1) {  // the last thread holds the totals
+          s_lrp[li] = racc;
+          // common case: every live triangle fits one round -> its bounds
+          // are known here, no serial round setup below
+          const int fast = li <= p.cap && racc <= (uint32_t)p.row_cap;
+          es.one_round = fast;
+          if (fast) {
+            es.round_end = li;
+            es.chunk_next = 0;
+            es.n_frag = 0;
+          }
+        }
       }
       __syncthreads();
       const int n_live = es.n_live;
+      const bool one_round = es.one_round != 0;
 
       // ---- phases 3/4: raster rounds over live triangles in index order ---
       for (int r0 = 0; r0 < n_live;) {
-        if (tid == 0) {
-          // live [r0, r1): at most cap triangles and row_cap bbox rows (a
-          // single triangle always fits: row_cap >= H); when several rounds
-          // are needed their triangle counts are balanced (a small last round
-          // cannot fill the CTA)
-          const int left = n_live - r0;
-          const int n_rounds = (left + p.cap - 1) / p.cap;
-          const int target = (left + n_rounds - 1) / n_rounds;
-          int lo = r0 + 1, hi = min(r0 + target, n_live);
-          const uint32_t base = s_lrp[r0];
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_lrp[mid] - base <= (uint32_t)p.row_cap) lo = mid; else hi = mid - 1;
+        if (!one_round) {  // serial round setup (records do not fit one round)
+          if (tid == 0) {
+            // live [r0, r1): at most cap triangles and row_cap bbox rows (a
+            // single triangle always fits: row_cap >= H); when several rounds
+            // are needed their triangle counts are balanced (a small last round
+            // cannot fill the CTA)
+            const int left = n_live - r0;
+            const int n_rounds = (left + p.cap - 1) / p.cap;
+            const int target = (left + n_rounds - 1) / n_rounds;
+            int lo = r0 + 1, hi = min(r0 + target, n_live);
+            const uint32_t base = s_lrp[r0];
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (s_lrp[mid] - base <= (uint32_t)p.row_cap) lo = mid; else hi = mid - 1;
+            }
+            es.round_end = lo;
+            es.chunk_next = 0;
+            es.n_frag = 0;
           }
-          es.round_end = lo;
-          es.chunk_next = 0;
-          es.n_frag = 0;
+          __syncthreads();
         }
-        __syncthreads();
         const int r1 = es.round_end;
         const uint32_t rbase = s_lrp[r0];
         const int n_rows = (int)(s_lrp[r1] - rbase);
