@@ -934,7 +934,7 @@ render_step_kernel(const RenderParams p) {
               // inclusive end is <= c (branch-free binary search over the scan)
               const int c = c0 + lane;
               int owner = 0;
-    #pragma unroll
+#pragma unroll
               for (int s = 16; s >= 1; s >>= 1) {
                 const int v = __shfl_sync(kFull, incl, owner + s - 1);
                 if (v <= c) owner += s;
@@ -951,13 +951,10 @@ render_step_kernel(const RenderParams p) {
                 pix = (uint32_t)((o_row - y0) * p.W + px);
                 cov = eval_exact(s_rec[o_tri], px, o_row, s_vxy64, s_viz, z);
               }
-              const uint32_t cm = __ballot_sync(kFull, cov);
-              if (cm == 0u) continue;
-              const int leader = __ffs(cm) - 1;
-              int slot = 0;
-              if (lane == leader) slot = atomicAdd(&es.n_frag, __popc(cm));
-              slot = __shfl_sync(kFull, slot, leader) + __popc(cm & lanemask_lt);
               if (cov) {
+                // a unique list slot per covered lane (ptxas aggregates the
+                // warp's increments into one shared atomic)
+                const int slot = atomicAdd(&es.n_frag, 1);
                 const float zf = (float)z;
                 const uint32_t zb = __float_as_uint(zf);
                 if (zb < atomicMin(&s_dbits[pix], zb)) atomicOr(&s_wkey[pix], kDecBit);
