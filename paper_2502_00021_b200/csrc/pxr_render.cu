@@ -189,7 +189,6 @@ struct EnvShared {
   int bias[2][3];
   int n_live;
   int round_end;
-  int chunk_next;
   int n_frag;
   int one_round;  // all live triangles of the band fit one raster round
   int plan_ok;
@@ -762,7 +761,6 @@ render_step_kernel(const RenderParams p) {
           es.one_round = fast;
           if (fast) {
             es.round_end = li;
-            es.chunk_next = 0;
             es.n_frag = 0;
           }
         }
@@ -789,7 +787,6 @@ render_step_kernel(const RenderParams p) {
               if (s_lrp[mid] - base <= (uint32_t)p.row_cap) lo = mid; else hi = mid - 1;
             }
             es.round_end = lo;
-            es.chunk_next = 0;
             es.n_frag = 0;
           }
           __syncthreads();
@@ -867,8 +864,8 @@ render_step_kernel(const RenderParams p) {
         }
         __syncthreads();
 
-        // (triangle, bbox row) units, 32 per chunk, chunks scheduled
-        // dynamically: each lane computes one row's conservative span and the
+        // (triangle, bbox row) units, 32 per chunk, chunks dealt round-robin
+        // to the warps: each lane computes one row's conservative span and the
         // non-empty spans go to the warp's queue; whenever 32 are queued (and
         // at the end) the warp expands 32 spans into pixel candidates and runs
         // the exact test on them, so the f64 work runs on full warps even
@@ -882,10 +879,9 @@ render_step_kernel(const RenderParams p) {
         uint2 *q = s_queue + warp * 64;
         int qn = 0;  // queued spans (warp-uniform)
         bool more = true;
+        int k = warp - kWarps;
         while (more) {
-          int k = 0;
-          if (lane == 0) k = atomicAdd(&es.chunk_next, 1);
-          k = __shfl_sync(kFull, k, 0);
+          k += kWarps;  // static round-robin over the chunks
           more = k < n_chunks;
           if (more) {
             const int u = k * 32 + lane;
