@@ -56,7 +56,7 @@
 
 namespace pxr {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 768;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLinks = 64;
 constexpr uint32_t kFull = 0xffffffffu;
