@@ -660,10 +660,20 @@ render_step_kernel(const RenderParams p) {
       const int per = (p.nt + kThreads - 1) / kThreads;
       const int t0 = min(tid * per, p.nt), t1 = min(t0 + per, p.nt);
       int my_live = 0, my_rows = 0;
+      int n0 = 0, n1 = 0, n2 = 0;  // indices of the next triangle, loaded one ahead
+      if (t0 < t1) {
+        n0 = __ldg(p.tris + 3 * t0 + 0);
+        n1 = __ldg(p.tris + 3 * t0 + 1);
+        n2 = __ldg(p.tris + 3 * t0 + 2);
+      }
       for (int t = t0; t < t1; t++) {
         uint32_t rows = 0;
-        const int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
-                  i2 = __ldg(p.tris + 3 * t + 2);
+        const int i0 = n0, i1 = n1, i2 = n2;
+        if (t + 1 < t1) {
+          n0 = __ldg(p.tris + 3 * t + 3);
+          n1 = __ldg(p.tris + 3 * t + 4);
+          n2 = __ldg(p.tris + 3 * t + 5);
+        }
         const float z0 = s_vz[i0], z1 = s_vz[i1], z2 = s_vz[i2];
         if (!(z0 < near_ || z1 < near_ || z2 < near_) && !(z0 > far_ && z1 > far_ && z2 > far_)) {
           const float2 a = s_vxy32[i0], b = s_vxy32[i1], c = s_vxy32[i2];
