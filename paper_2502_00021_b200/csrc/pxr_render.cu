@@ -1052,7 +1052,33 @@ render_step_kernel(const RenderParams p) {
       }
       const bool row_groups = (p.W & 3) == 0;  // a 4-pixel group never wraps a row
       const int ngroups = npx >> 2;
-      for (int gi = tid; gi < ngroups; gi += kThreads) {
+      // video RGB through the byte-permute plan without a depth output (the
+      // env-step path): a dedicated loop without the per-group mode checks
+      const bool fast = plan_ok && !p.gray && p.out_depth == nullptr;
+      if (fast) {
+        for (int gi = tid; gi < ngroups; gi += kThreads) {
+          const float4 d4 = reinterpret_cast<const float4 *>(s_depth)[gi];
+          uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
+          const int i0 = gi << 2;
+          const int y = (int)__umulhi((uint32_t)i0, p.wmagic);
+          const uint4 pl = s_gplan[(i0 - y * p.W) >> 2];
+          const uint32_t *src =
+              reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y0 + y]) + pl.x;
+          const bool b0 = isinf(d4.x), b1 = isinf(d4.y), b2 = isinf(d4.z), b3 = isinf(d4.w);
+          const uint32_t m0 = (b0 ? 0x00ffffffu : 0u) | (b1 ? 0xff000000u : 0u);
+          const uint32_t m1 = (b1 ? 0x0000ffffu : 0u) | (b2 ? 0xffff0000u : 0u);
+          const uint32_t m2 = (b2 ? 0x000000ffu : 0u) | (b3 ? 0xffffff00u : 0u);
+          const uint32_t *w0 = src + (pl.y >> 16), *w1 = src + (pl.z >> 16),
+                         *w2 = src + (pl.w >> 16);
+          const uint32_t t0 = __byte_perm(w0[0], w0[1], pl.y & 0xffffu);
+          const uint32_t t1 = __byte_perm(w1[0], w1[1], pl.z & 0xffffu);
+          const uint32_t t2 = __byte_perm(w2[0], w2[1], pl.w & 0xffffu);
+          c3[0] = (t0 & m0) | (c3[0] & ~m0);
+          c3[1] = (t1 & m1) | (c3[1] & ~m1);
+          c3[2] = (t2 & m2) | (c3[2] & ~m2);
+        }
+      }
+      for (int gi = fast ? ngroups : tid; gi < ngroups; gi += kThreads) {
         const int i0 = gi << 2;
         const float4 d4 = reinterpret_cast<const float4 *>(s_depth)[gi];
         const float d[4] = {d4.x, d4.y, d4.z, d4.w};
