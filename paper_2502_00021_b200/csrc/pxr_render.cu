@@ -8,27 +8,29 @@
 //   advance_distractors + auto-reset re-draw    distractor.py:116-137, env.py:239-244
 //   _color_kernel / _video_kernel               distractor.py:140-176
 //
-// Design (B200-first). Persistent CTAs of 16 warps,
+// Design (B200-first). Persistent CTAs of 24 warps,
 // one env per CTA iteration, every intermediate in shared memory, every
-// phase a flat, balanced loop over the CTA:
-//   0. per-link glibc-exact cosf/sinf; distractor state for 32 envs at a
-//      time (one lane per env); the env's video frame is fetched into shared
-//      memory by a TMA bulk copy (cp.async.bulk + mbarrier);
+// phase a flat loop over the CTA:
+//   0. the env's video frame is fetched into shared memory by a TMA bulk
+//      copy (cp.async.bulk + mbarrier); its per-link glibc-exact cosf/sinf
+//      and distractor state (32 envs at a time, one lane per env) were
+//      prepared by one warp during the previous env's rasterisation;
 //   1. world transform + projection of every vertex (f32 like the
 //      reference; f64 copies and 1/z for the raster);
 //   2. triangle liveness exactly as the reference culls (near/far, zero
-//      area, empty pixel bbox, degenerate normal); a block scan over the
-//      triangles in index order gives live index + bbox-row prefix; sky /
-//      floor background under an empty z-buffer;
-//   3. per round of live triangles (all of them at 84x84): a record per
-//      triangle (f64 edge coefficients, exact reciprocal of the area, flat
-//      colour) plus f32 line equations for conservative row spans; then the
-//      (triangle, bbox row) units, flat over the warps: each lane computes
-//      one row's conservative span, the warp expands its 32 spans into
-//      pixel candidates (warp scan + start-mask owner search) and runs the
-//      reference's exact f64 edge / barycentric / depth arithmetic on them;
-//      covered fragments min-reduce their f32 depth per pixel with a 32-bit
-//      shared-memory atomicMin and are appended to a fragment list;
+//      area, empty pixel bbox); a block scan over the triangles in index
+//      order gives live index + bbox-row prefix; the background (sky, floor,
+//      video texel) under an empty z-buffer, written as final colours;
+//   3. per round of live triangles (one round whenever the records fit): a
+//      record per triangle (edge vectors, exact reciprocal of the area, flat
+//      colour, the degenerate-normal cull) plus f32 line equations for
+//      conservative row spans; (triangle, bbox row) units in 32-row chunks
+//      dealt to the warps: each lane computes one row's conservative span,
+//      non-empty spans gather in a per-warp queue and every 32 are expanded
+//      into pixel candidates (warp scan + owner search) for the reference's
+//      exact f64 edge / barycentric / depth arithmetic; covered fragments
+//      min-reduce their f32 depth per pixel with a 32-bit shared-memory
+//      atomicMin and are appended to a fragment list;
 //   4. exact order-independent resolve of the reference's SEQUENTIAL strict
 //      z-test (render.py:452, triangles in index order, f64 z compared with
 //      the f32 z-buffer): with F = min over fragments of RN32(z) and
@@ -38,10 +40,15 @@
 //      previous content. (D only decreases; the first member of S always
 //      writes when F < d0; later members write iff z < F; nothing outside S
 //      can.) One atomicMax over key = (z < F) ? 0x10000 + i : 0xFFFF - i
-//      encodes both cases; bit 31 of the same word records F < d0;
-//   5. composite (video texel from shared memory or colour clamp-add,
-//      grayscale) into a shared-memory frame stored with one TMA bulk copy
-//      overlapped with the next env.
+//      encodes both cases; bit 31 of the same word records F < d0. The
+//      winners paint their final colour;
+//   5. the frame (RGB or grayscale) leaves shared memory in one TMA bulk
+//      store overlapped with the next env.
+// Final colours: every pixel is written last either by the background (2) or
+// by a winner's paint (4), and the distractor composite + grayscale
+// (distractor.py:140-176, env.py:168-173) is a per-pixel function of that
+// colour, so it is applied where the colour is written (emit) -- there is no
+// separate composite pass.
 // Compiled with -fmad=false: no FMA contraction, every f32/f64 operation
 // rounds where numba's code does. The only FMAs are explicit
 // (__fma_rn / __fmaf_rn): the glibc sinf/cosf restatement, the exact
@@ -649,6 +656,29 @@ render_step_kernel(const RenderParams p) {
       const int y0 = kBands ? yb : 0;  // compile-time 0 for one band
       const int y1 = kBands ? min(y0 + band_h, p.H) : p.H;
       const int npx = (y1 - y0) * p.W;  // pixels of this band
+      const uint8_t *vsrc = p.mode == PXR_MODE_VIDEO
+                                ? (p.vframe_bulk ? s_vframe
+                                                 : p.frames + es.frame_idx[cb] * p.vframe_bytes)
+                                : nullptr;
+      // colour distractor as a per-byte saturating add/sub on the packed RGB
+      // word (__vaddus4 / __vsubus4 == clamp(v + b, 0, 255) for |b| <= 255)
+      uint32_t bpos = 0u, bneg = 0u;
+      if (p.mode == PXR_MODE_COLOR) {
+        for (int ch = 0; ch < 3; ch++) {
+          const int bc = es.bias[cb][ch];
+          bpos |= (uint32_t)(bc > 0 ? bc : 0) << (8 * ch);
+          bneg |= (uint32_t)(bc < 0 ? -bc : 0) << (8 * ch);
+        }
+      }
+      // a pixel's final colour: colour distractor, then grayscale
+      auto emit = [&](uint32_t pix, uint32_t rgb) {
+        if (p.mode == PXR_MODE_COLOR) rgb = __vsubus4(__vaddus4(rgb, bpos), bneg);
+        if (p.gray)
+          s_gray[pix] = (uint8_t)((299u * (rgb & 0xffu) + 587u * ((rgb >> 8) & 0xffu) +
+                                   114u * ((rgb >> 16) & 0xffu) + 500u) / 1000u);
+        else
+          put_rgb(s_col, pix, rgb);
+      };
       if (kBands && y0 > 0) {  // the previous band's TMA store must have finished reading
         if (tid == 0 && p.use_bulk) bulk_wait_read();
         __syncthreads();
@@ -695,18 +725,34 @@ render_step_kernel(const RenderParams p) {
         my_live += rows != 0u;
         my_rows += (int)rows;
       }
-      // background: sky / floor under an empty z-buffer (render.py:306-344)
-      if (p.mode == PXR_MODE_VIDEO && !p.draw_floor) {
-        // the background colour is never read: every inf pixel takes the video
+      // background: sky / floor under an empty z-buffer (render.py:306-344),
+      // written as FINAL colours: a pixel's colour is written last either here
+      // or by the resolve's paint, and the distractor composite + grayscale
+      // is a per-pixel function of that colour (distractor.py:140-176,
+      // env.py:168-173) -- so it is applied at write time (emit) and there is
+      // no separate composite pass. Video: inf pixels take the texel.
+      if (y0 == 0) {  // the env's video frame (one fetch for all bands)
+        if (p.mode == PXR_MODE_VIDEO && p.vframe_bulk) mbar_wait_parity(&es.vbar, vphase);
+        vphase ^= 1u;
+      }
+      if (p.mode == PXR_MODE_VIDEO && !p.draw_floor && plan_ok && !p.gray) {
+        // 4-pixel groups: three texel words through the byte-permute plan
         const float inf = __int_as_float(0x7f800000);
-        const int n4 = npx >> 2;
-        for (int i = tid; i < n4; i += kThreads) {
-          reinterpret_cast<float4 *>(s_depth)[i] = make_float4(inf, inf, inf, inf);
-          reinterpret_cast<uint4 *>(s_wkey)[i] = make_uint4(0u, 0u, 0u, 0u);
-        }
-        for (int i = (n4 << 2) + tid; i < npx; i += kThreads) {
-          s_depth[i] = inf;
-          s_wkey[i] = 0u;
+        const int n4 = npx >> 2;  // plan_ok: W % 4 == 0, no tail
+        for (int gi = tid; gi < n4; gi += kThreads) {
+          const int i0 = gi << 2;
+          const int yb = (int)__umulhi((uint32_t)i0, p.wmagic);
+          const uint4 pl = s_gplan[(i0 - yb * p.W) >> 2];
+          const uint32_t *src =
+              reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y0 + yb]) + pl.x;
+          const uint32_t *w0 = src + (pl.y >> 16), *w1 = src + (pl.z >> 16),
+                         *w2 = src + (pl.w >> 16);
+          uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
+          c3[0] = __byte_perm(w0[0], w0[1], pl.y & 0xffffu);
+          c3[1] = __byte_perm(w1[0], w1[1], pl.z & 0xffffu);
+          c3[2] = __byte_perm(w2[0], w2[1], pl.w & 0xffffu);
+          reinterpret_cast<float4 *>(s_depth)[gi] = make_float4(inf, inf, inf, inf);
+          reinterpret_cast<uint4 *>(s_wkey)[gi] = make_uint4(0u, 0u, 0u, 0u);
         }
       } else {
         for (int i = tid; i < npx; i += kThreads) {
@@ -727,9 +773,13 @@ render_step_kernel(const RenderParams p) {
             const double *r = p.floor_rays + ((int64_t)y0 * p.W + i) * 3;
             floor_px(p, ex, ez, r[0], r[1], r[2], d, c);
           }
+          if (p.mode == PXR_MODE_VIDEO && isinf(d)) {  // distractor.py:172-176
+            const uint8_t *t = vsrc + s_rowmap[y] + s_colmap[x];
+            c = (uint32_t)t[0] | ((uint32_t)t[1] << 8) | ((uint32_t)t[2] << 16);
+          }
           s_depth[i] = d;
-          put_rgb(s_col, (uint32_t)i, c);
           s_wkey[i] = 0u;
+          emit((uint32_t)i, c);
         }
       }
       // block scan over triangles in index order: live ids, bbox-row prefix
@@ -987,7 +1037,7 @@ render_step_kernel(const RenderParams p) {
           __syncthreads();
           for (int i = tid; i < n_frag; i += kThreads) {
             const uint32_t pix = s_frag[i].y & 0xFFFFFu, tri = s_frag[i].y >> 20;
-            if (resolve_winner(s_wkey[pix]) == (int)tri) put_rgb(s_col, pix, s_rec[tri].rgb);
+            if (resolve_winner(s_wkey[pix]) == (int)tri) emit(pix, s_rec[tri].rgb);
           }
           if (r1 < n_live) {
             __syncthreads();
@@ -1015,7 +1065,7 @@ render_step_kernel(const RenderParams p) {
                   atomicMax(&s_wkey[pix],
                             hb | (z < (double)__uint_as_float(F) ? 0x10000u + j : 0xFFFFu - j));
                 } else if (resolve_winner(s_wkey[pix]) == j) {
-                  put_rgb(s_col, pix, R.rgb);
+                  emit(pix, R.rgb);
                 }
               }
             }
@@ -1030,153 +1080,14 @@ render_step_kernel(const RenderParams p) {
       if (warp == kWarps - 1 && !prepared)  // env without live triangles
         prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es, lane);
 
-      // ---- phase 5: composite + postprocess (distractor.py:140-176, env.py:168-173)
-      if (y0 == 0) {  // the env's video frame (one fetch for all bands)
-        if (p.mode == PXR_MODE_VIDEO && p.vframe_bulk) mbar_wait_parity(&es.vbar, vphase);
-        vphase ^= 1u;
-      }
-      const uint8_t *vsrc = p.mode == PXR_MODE_VIDEO
-                                ? (p.vframe_bulk ? s_vframe
-                                                 : p.frames + es.frame_idx[cb] * p.vframe_bytes)
-                                : nullptr;
-      // Four consecutive pixels per thread: 12 colour bytes are three aligned
-      // words; the colour bias is a per-byte saturating add/sub (__vaddus4 /
-      // __vsubus4 == clamp(v + b, 0, 255) for |b| <= 255).
-      uint32_t bpos[3] = {0u, 0u, 0u}, bneg[3] = {0u, 0u, 0u};
-      if (p.mode == PXR_MODE_COLOR) {
-        for (int byte = 0; byte < 12; byte++) {
-          const int bc = es.bias[cb][byte % 3];
-          bpos[byte >> 2] |= (uint32_t)(bc > 0 ? bc : 0) << (8 * (byte & 3));
-          bneg[byte >> 2] |= (uint32_t)(bc < 0 ? -bc : 0) << (8 * (byte & 3));
-        }
-      }
-      const bool row_groups = (p.W & 3) == 0;  // a 4-pixel group never wraps a row
-      const int ngroups = npx >> 2;
-      // video RGB through the byte-permute plan without a depth output (the
-      // env-step path): a dedicated loop without the per-group mode checks
-      const bool fast = plan_ok && !p.gray && p.out_depth == nullptr;
-      if (fast) {
-        for (int gi = tid; gi < ngroups; gi += kThreads) {
-          const float4 d4 = reinterpret_cast<const float4 *>(s_depth)[gi];
-          uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
-          const int i0 = gi << 2;
-          const int y = (int)__umulhi((uint32_t)i0, p.wmagic);
-          const uint4 pl = s_gplan[(i0 - y * p.W) >> 2];
-          const uint32_t *src =
-              reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y0 + y]) + pl.x;
-          const bool b0 = isinf(d4.x), b1 = isinf(d4.y), b2 = isinf(d4.z), b3 = isinf(d4.w);
-          const uint32_t m0 = (b0 ? 0x00ffffffu : 0u) | (b1 ? 0xff000000u : 0u);
-          const uint32_t m1 = (b1 ? 0x0000ffffu : 0u) | (b2 ? 0xffff0000u : 0u);
-          const uint32_t m2 = (b2 ? 0x000000ffu : 0u) | (b3 ? 0xffffff00u : 0u);
-          const uint32_t *w0 = src + (pl.y >> 16), *w1 = src + (pl.z >> 16),
-                         *w2 = src + (pl.w >> 16);
-          const uint32_t t0 = __byte_perm(w0[0], w0[1], pl.y & 0xffffu);
-          const uint32_t t1 = __byte_perm(w1[0], w1[1], pl.z & 0xffffu);
-          const uint32_t t2 = __byte_perm(w2[0], w2[1], pl.w & 0xffffu);
-          c3[0] = (t0 & m0) | (c3[0] & ~m0);
-          c3[1] = (t1 & m1) | (c3[1] & ~m1);
-          c3[2] = (t2 & m2) | (c3[2] & ~m2);
-        }
-      }
-      for (int gi = fast ? ngroups : tid; gi < ngroups; gi += kThreads) {
-        const int i0 = gi << 2;
-        const float4 d4 = reinterpret_cast<const float4 *>(s_depth)[gi];
-        const float d[4] = {d4.x, d4.y, d4.z, d4.w};
-        const bool bg[4] = {isinf(d4.x), isinf(d4.y), isinf(d4.z), isinf(d4.w)};
-        uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
-        uint32_t w[3];
-        const bool video = p.mode == PXR_MODE_VIDEO;
-        w[0] = c3[0]; w[1] = c3[1]; w[2] = c3[2];
-        if (plan_ok) {  // branch-free: texel words merged under per-pixel byte masks
-          const int y = (int)__umulhi((uint32_t)i0, p.wmagic);
-          const int x = i0 - y * p.W;
-          const uint4 pl = s_gplan[x >> 2];
-          const uint32_t *src =
-              reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y0 + y]) + pl.x;
-          const uint32_t sels[3] = {pl.y, pl.z, pl.w};
-          const uint32_t m[3] = {
-              (bg[0] ? 0x00ffffffu : 0u) | (bg[1] ? 0xff000000u : 0u),
-              (bg[1] ? 0x0000ffffu : 0u) | (bg[2] ? 0xffff0000u : 0u),
-              (bg[2] ? 0x000000ffu : 0u) | (bg[3] ? 0xffffff00u : 0u)};
-#pragma unroll
-          for (int q = 0; q < 3; q++) {
-            const uint32_t *wp = src + (sels[q] >> 16);
-            const uint32_t t = __byte_perm(wp[0], wp[1], sels[q] & 0xffffu);
-            w[q] = (t & m[q]) | (w[q] & ~m[q]);
-          }
-        } else if (video && (bg[0] | bg[1] | bg[2] | bg[3])) {  // distractor.py:172-176
-          int y = (int)__umulhi((uint32_t)i0, p.wmagic);
-          int x = i0 - y * p.W;
-          y += y0;  // frame row
-          if (p.vframe_bulk && row_groups) {
-            const uint32_t rb = s_rowmap[y];
-            const uint4 cm = *reinterpret_cast<const uint4 *>(s_colmap + x);
-            const uint32_t cms[4] = {cm.x, cm.y, cm.z, cm.w};
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-              if (!bg[k]) continue;
-              const uint32_t off = rb + cms[k];  // 24-bit texel from two aligned words
-              const uint32_t *wp = reinterpret_cast<const uint32_t *>(s_vframe + (off & ~3u));
-              put_texel(w, k, __funnelshift_r(wp[0], wp[1], 8 * (off & 3u)) & 0xffffffu);
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-              if (bg[k]) {
-                const uint8_t *src = vsrc + s_rowmap[y] + s_colmap[x];
-                put_texel(w, k, (uint32_t)src[0] | ((uint32_t)src[1] << 8) |
-                                    ((uint32_t)src[2] << 16));
-              }
-              if (++x == p.W) { x = 0; y++; }
-            }
-          }
-        } else if (p.mode == PXR_MODE_COLOR) {  // distractor.py:149-161
-          for (int q = 0; q < 3; q++) w[q] = __vsubus4(__vaddus4(w[q], bpos[q]), bneg[q]);
-        }
-        if (p.gray) {  // env.py:168-173
-          uint32_t gw = 0;
-#pragma unroll
-          for (int k = 0; k < 4; k++) {
-            uint32_t ch3[3];
-#pragma unroll
-            for (int ch = 0; ch < 3; ch++) {
-              const int byte = 3 * k + ch;
-              ch3[ch] = (w[byte >> 2] >> (8 * (byte & 3))) & 0xffu;
-            }
-            gw |= ((299u * ch3[0] + 587u * ch3[1] + 114u * ch3[2] + 500u) / 1000u) << (8 * k);
-          }
-          reinterpret_cast<uint32_t *>(s_gray)[gi] = gw;
-        } else {
-          c3[0] = w[0]; c3[1] = w[1]; c3[2] = w[2];
-        }
-        if (p.out_depth != nullptr) {
-          float *dd = p.out_depth + (int64_t)env * fpx + (int64_t)y0 * p.W + i0;
-          if (p.depth_vec) *reinterpret_cast<float4 *>(dd) = d4;
-          else for (int k = 0; k < 4; k++) dd[k] = d[k];
-        }
-      }
-      for (int i = (ngroups << 2) + tid; i < npx; i += kThreads) {  // tail pixels
-        const float d = s_depth[i];
-        uint32_t rgb = s_col[3 * i] | (s_col[3 * i + 1] << 8) | (s_col[3 * i + 2] << 16);
-        if (p.mode == PXR_MODE_VIDEO && isinf(d)) {
-          const int y = (int)__umulhi((uint32_t)i, p.wmagic), x = i - y * p.W;
-          const uint8_t *src = vsrc + s_rowmap[y0 + y] + s_colmap[x];
-          rgb = (uint32_t)src[0] | ((uint32_t)src[1] << 8) | ((uint32_t)src[2] << 16);
-        } else if (p.mode == PXR_MODE_COLOR) {
-          uint32_t o = 0;
-          for (int ch = 0; ch < 3; ch++) {
-            const int v = (int)((rgb >> (8 * ch)) & 0xffu) + es.bias[cb][ch];
-            o |= (uint32_t)min(255, max(0, v)) << (8 * ch);
-          }
-          rgb = o;
-        }
-        if (p.gray) {
-          s_gray[i] = (uint8_t)((299u * (rgb & 0xffu) + 587u * ((rgb >> 8) & 0xffu) +
-                                 114u * ((rgb >> 16) & 0xffu) + 500u) / 1000u);
-        } else {
-          put_rgb(s_col, (uint32_t)i, rgb);
-        }
-        if (p.out_depth != nullptr) p.out_depth[(int64_t)env * fpx + (int64_t)y0 * p.W + i] = d;
+      // ---- phase 5: depth output (debug / _render_frame parity only) ------
+      if (p.out_depth != nullptr) {
+        float *dd = p.out_depth + (int64_t)env * fpx + (int64_t)y0 * p.W;
+        if (p.depth_vec)
+          for (int gi = tid; gi < (npx >> 2); gi += kThreads)
+            reinterpret_cast<float4 *>(dd)[gi] = reinterpret_cast<const float4 *>(s_depth)[gi];
+        for (int i = p.depth_vec ? ((npx >> 2) << 2) + tid : tid; i < npx; i += kThreads)
+          dd[i] = s_depth[i];
       }
 
       // ---- phase 6: frame -> HBM (one TMA bulk store) --------------------
