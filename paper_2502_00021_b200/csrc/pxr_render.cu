@@ -380,20 +380,15 @@ __device__ __forceinline__ void span_setup(const float2 a, const float2 b, const
   for (int k = 0; k < 3; k++) {
     const float2 s = v[k], t = v[(k + 1) % 3];
     const float A = t.x - s.x, B = t.y - s.y;
-    if (B != 0.0f) {
-      // the slope only feeds a conservative bound: __fdividef's <= 2 ulp
-      // error moves the line by <= 2^-22 |r| (H + |s.y|), far inside m
-      const float r = __fdividef(A, B);
-      S.r[k] = r;
-      S.c0[k] = __fmaf_rn(-r, s.y, s.x);
-      S.m[k] = 0x1p-10f + (fabsf(s.x) + fabsf(r) * (fabsf(s.y) + ymax)) * 0x1p-17f;
-      kinds |= (B > 0.0f ? 0u : 1u) << (2 * k);
-    } else {  // horizontal edge: only the sign of A * (y - s.y) matters
-      S.r[k] = 0.0f;
-      S.c0[k] = s.y;
-      S.m[k] = 0.0f;
-      kinds |= (A > 0.0f ? 2u : 3u) << (2 * k);
-    }
+    // horizontal edge (B == 0): only the sign of A * (y - s.y) matters; else
+    // an x bound whose slope only feeds a conservative bound: __fdividef's
+    // <= 2 ulp error moves the line by <= 2^-22 |r| (H + |s.y|), far inside m
+    const bool hz = B == 0.0f;
+    const float r = hz ? 0.0f : __fdividef(A, B);
+    S.r[k] = r;
+    S.c0[k] = hz ? s.y : __fmaf_rn(-r, s.y, s.x);
+    S.m[k] = hz ? 0.0f : 0x1p-10f + (fabsf(s.x) + fabsf(r) * (fabsf(s.y) + ymax)) * 0x1p-17f;
+    kinds |= (hz ? (A > 0.0f ? 2u : 3u) : (B > 0.0f ? 0u : 1u)) << (2 * k);
   }
   S.kinds = (uint16_t)kinds;
 }
