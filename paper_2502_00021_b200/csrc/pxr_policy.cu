@@ -20,56 +20,93 @@ namespace pxr {
 constexpr int kPolThreads = 128;
 constexpr int kK = 8, kS = 4, kF = 16;
 constexpr int kMaxJoints = 32;
+constexpr int kStrip = 4;  // output positions per thread step
 
 __global__ void __launch_bounds__(kPolThreads)
 conv_stub_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W, int C,
                  const float *__restrict__ conv, const float *__restrict__ proj, int J,
-                 double *__restrict__ out) {
+                 double *__restrict__ out, int bulk) {
   extern __shared__ __align__(16) unsigned char sm[];
   float *s_w = reinterpret_cast<float *>(sm);          // (K*K*C, 16): row (ky, kx, c)
-  uint8_t *s_obs = sm + kK * kK * C * kF * sizeof(float);
+  uint8_t *s_obs0 = sm + kK * kK * C * kF * sizeof(float);  // two frame buffers
   __shared__ float s_red[kPolThreads / 32][kMaxJoints];
+  __shared__ uint64_t s_bar[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int oh = (H - kK) / kS + 1, ow = (W - kK) / kS + 1;
   const int nw = kK * kK * C * kF;
   const int frame = H * W * C;
   const float inv = 1.0f / 255.0f;  // float32(1/255), bench.py:101
+  const int fstride = (frame + 15) & ~15;
   for (int i = tid; i < nw; i += kPolThreads) s_w[i] = conv[i];
-  for (int64_t env = blockIdx.x; env < batch; env += gridDim.x) {
-    __syncthreads();  // weights loaded / previous env's frame no longer read
-    const uint8_t *src = obs + env * (int64_t)frame;
-    for (int i = tid; i < frame; i += kPolThreads) s_obs[i] = src[i];
-    __syncthreads();
+  // frames arrive by TMA bulk copy, the next env's while this one is
+  // convolved (bulk: frame size and base 16-byte aligned), else byte loads
+  if (bulk && tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+    if (blockIdx.x < batch) {
+      mbar_arrive_expect_tx(&s_bar[0], (uint32_t)frame);
+      bulk_load_g2s(s_obs0, obs + (int64_t)blockIdx.x * frame, (uint32_t)frame, &s_bar[0]);
+    }
+  }
+  int it = 0;
+  for (int64_t env = blockIdx.x; env < batch; env += gridDim.x, it++) {
+    __syncthreads();  // weights loaded / the other buffer no longer read
+    uint8_t *s_obs = s_obs0 + (it & 1) * fstride;
+    if (bulk) {
+      const int64_t nxt = env + gridDim.x;
+      if (tid == 0 && nxt < batch) {
+        uint64_t *bar = &s_bar[(it + 1) & 1];
+        mbar_arrive_expect_tx(bar, (uint32_t)frame);
+        bulk_load_g2s(s_obs0 + ((it + 1) & 1) * fstride, obs + nxt * frame, (uint32_t)frame, bar);
+      }
+      mbar_wait_parity(&s_bar[it & 1], (uint32_t)((it >> 1) & 1));
+    } else {
+      const uint8_t *src = obs + env * (int64_t)frame;
+      for (int i = tid; i < frame; i += kPolThreads) s_obs[i] = src[i];
+      __syncthreads();
+    }
     float pacc[kMaxJoints];
 #pragma unroll
     for (int j = 0; j < kMaxJoints; j++) pacc[j] = 0.0f;
-    for (int pos = tid; pos < oh * ow; pos += kPolThreads) {
-      const int oy = pos / ow, ox = pos - oy * ow;
-      float acc[kF];
+    // each thread owns strips of kStrip adjacent output positions (same oy):
+    // one broadcast load of a weight row feeds kStrip x 16 FMAs
+    const int strips_x = (ow + kStrip - 1) / kStrip;
+    for (int st = tid; st < oh * strips_x; st += kPolThreads) {
+      const int oy = st / strips_x, ox0 = (st - oy * strips_x) * kStrip;
+      const int nx = min(kStrip, ow - ox0);
+      float acc[kStrip][kF];
 #pragma unroll
-      for (int f = 0; f < kF; f++) acc[f] = 0.0f;
+      for (int i = 0; i < kStrip; i++)
+#pragma unroll
+        for (int f = 0; f < kF; f++) acc[i][f] = 0.0f;
       for (int ky = 0; ky < kK; ky++) {
-        const uint8_t *row = s_obs + ((oy * kS + ky) * W + ox * kS) * C;
+        const uint8_t *row = s_obs + ((oy * kS + ky) * W + ox0 * kS) * C;
         for (int kc = 0; kc < kK * C; kc++) {  // (kx, c) in memory order
-          const float x = (float)row[kc] * inv;
           const float4 *w4 = reinterpret_cast<const float4 *>(s_w + (ky * kK * C + kc) * kF);
+          const float4 wa = w4[0], wb = w4[1], wc = w4[2], wd = w4[3];  // broadcast
+          const float w[kF] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w,
+                               wc.x, wc.y, wc.z, wc.w, wd.x, wd.y, wd.z, wd.w};
 #pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const float4 w = w4[q];  // same address in every lane: broadcast
-            acc[4 * q + 0] = __fmaf_rn(x, w.x, acc[4 * q + 0]);
-            acc[4 * q + 1] = __fmaf_rn(x, w.y, acc[4 * q + 1]);
-            acc[4 * q + 2] = __fmaf_rn(x, w.z, acc[4 * q + 2]);
-            acc[4 * q + 3] = __fmaf_rn(x, w.w, acc[4 * q + 3]);
+          for (int i = 0; i < kStrip; i++) {
+            // positions past the edge read in-bounds pixels and are dropped
+            const float x = (float)row[(i < nx ? i : 0) * kS * C + kc] * inv;
+#pragma unroll
+            for (int f = 0; f < kF; f++) acc[i][f] = __fmaf_rn(x, w[f], acc[i][f]);
           }
         }
       }
-      const float *pr = proj + (int64_t)pos * kF * J;
 #pragma unroll
-      for (int f = 0; f < kF; f++) {
-        const float v = acc[f] > 0.0f ? acc[f] : 0.0f;  // ReLU
+      for (int i = 0; i < kStrip; i++) {
+        if (i >= nx) break;
+        const float *pr = proj + (int64_t)(oy * ow + ox0 + i) * kF * J;
 #pragma unroll
-        for (int j = 0; j < kMaxJoints; j++)
-          if (j < J) pacc[j] = __fmaf_rn(v, __ldg(pr + f * J + j), pacc[j]);
+        for (int f = 0; f < kF; f++) {
+          const float v = acc[i][f] > 0.0f ? acc[i][f] : 0.0f;  // ReLU
+#pragma unroll
+          for (int j = 0; j < kMaxJoints; j++)
+            if (j < J) pacc[j] = __fmaf_rn(v, __ldg(pr + f * J + j), pacc[j]);
+        }
       }
     }
     // fixed-order reduction: xor tree inside the warp, warps in index order
@@ -105,7 +142,9 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   if (channels < 1 || channels > 4) return set_invalid("channels must be 1..4");
   if (n_joints < 1 || n_joints > kMaxJoints) return set_unsupported("n_joints must be 1..32");
   if (batch == 0) return PXR_OK;
-  const int smem = kK * kK * channels * kF * (int)sizeof(float) + height * width * channels;
+  const int frame = height * width * channels;
+  const int bulk = (frame % 16 == 0) && ((reinterpret_cast<uintptr_t>(obs) & 15) == 0);
+  const int smem = kK * kK * channels * kF * (int)sizeof(float) + 2 * ((frame + 15) & ~15);
   if (smem > 200 * 1024) return set_unsupported("observation too large for the policy kernel");
   cudaError_t e = cudaFuncSetAttribute(conv_stub_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -118,6 +157,6 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   const int64_t cap = (int64_t)sms * per_sm;
   const int grid = (int)(batch < cap ? batch : cap);
   conv_stub_kernel<<<grid, kPolThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-      obs, batch, height, width, channels, conv, proj, n_joints, out);
+      obs, batch, height, width, channels, conv, proj, n_joints, out, bulk);
   return check_launch("conv_stub_kernel");
 }
