@@ -230,11 +230,12 @@ pxr_status pxr_forward_kinematics(const double *qpos, const int32_t *parent,
  * tanh(relu(conv16x8x8s4(obs * f32(1/255))) @ proj), f32 arithmetic.
  * conv: f32 (8*8*C, 16), row (ky, kx, c); proj: f32 (oh*ow*16, J), feature
  * order (oy, ox, f). Each batch row is computed independently of the batch
- * (bench.py:131-145 contract). J <= 32. */
+ * (bench.py:131-145 contract). J <= 32. workspace: f32 device scratch of
+ * batch * oh * ow * 16 floats (the ReLU'd features). */
 pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, int32_t height,
                                  int32_t width, int32_t channels, const float *conv,
                                  const float *proj, int32_t n_joints, double *out,
-                                 void *stream);
+                                 float *workspace, void *stream);
 
 #ifdef __cplusplus
 }

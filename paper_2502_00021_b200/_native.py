@@ -145,7 +145,8 @@ def lib() -> ctypes.CDLL:
     L.pxr_forward_kinematics.restype = _i32
     L.pxr_forward_kinematics.argtypes = [_vp, _vp, _vp, _i32, _i64, _vp, _vp]
     L.pxr_conv_stub_forward.restype = _i32
-    L.pxr_conv_stub_forward.argtypes = [_vp, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _vp]
+    L.pxr_conv_stub_forward.argtypes = [_vp, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
+                                        _vp]
     L.pxr_physics_step.restype = _i32
     L.pxr_physics_step.argtypes = [P(Model), _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]
     L.pxr_reset_envs.restype = _i32

@@ -4,8 +4,9 @@ Mirrors ``pixelctrl.bench`` (/root/reference/pkg/src/pixelctrl/bench.py):
 ``ConvStub`` / ``conv_stub_forward`` (36-145), ``BenchConfig`` /
 ``BenchRecord`` / ``run_benchmark`` (148-236) and the CSV format (239-277).
 The policy forward runs in ``pxr_conv_stub_forward`` (csrc/pxr_policy.cu):
-one CTA per env, so a row never depends on its batch; observations, actions
-and the env state stay on the device through the whole loop. The repo-root
+a per-env convolution kernel and a fixed-order projection kernel, so a row
+never depends on its batch; observations, actions and the env state stay on
+the device through the whole loop. The repo-root
 ``bench.py`` is the driver's render benchmark; this module is the
 reference's env-step sweep.
 """
@@ -105,10 +106,11 @@ def conv_stub_forward(stub: ConvStub, obs, threads: int = 1):
     x = x.to(device=dev, dtype=torch.uint8).contiguous()
     conv, proj = stub.device_weights(dev)
     out = torch.empty((shape[0], stub.n_joints), dtype=torch.float64, device=dev)
+    ws = torch.empty((max(shape[0], 1), stub.proj.shape[0]), dtype=torch.float32, device=dev)
     with torch.cuda.device(dev):
         _native.check(_native.lib().pxr_conv_stub_forward(
             x.data_ptr(), shape[0], stub.height, stub.width, stub.channels, conv.data_ptr(),
-            proj.data_ptr(), stub.n_joints, out.data_ptr(), _native.stream_ptr()))
+            proj.data_ptr(), stub.n_joints, out.data_ptr(), ws.data_ptr(), _native.stream_ptr()))
     return out.cpu().numpy() if host else out
 
 

@@ -3,10 +3,12 @@
 // obs / 255, ReLU, linear projection of the (oy, ox, f)-ordered features,
 // tanh.
 //
-// One CTA per env (grid-stride over envs), so a batch row never depends on
-// the batch it is in (reference tests/test_bench.py:92-98): every thread
-// owns fixed conv output positions and all 16 filters of each, and the
-// projection partial sums are reduced in a fixed tree. f32 arithmetic like
+// Two kernels: the convolution (one CTA per env, frames by double-buffered
+// TMA bulk copies, each thread a strip of 4 output positions x 16 filters)
+// writes ReLU'd features to a workspace; the projection (one warp per env,
+// proj tiles in shared memory shared by 8 envs) reduces them in a fixed
+// order. A batch row therefore never depends on the batch it is in
+// (reference tests/test_bench.py:92-98). f32 arithmetic like
 // the reference's f32 BLAS path; accuracy is checked against a float64
 // evaluation (<= 1e-5, tests/test_bench.py:56-68).
 #include <cuda_runtime.h>
@@ -24,12 +26,10 @@ constexpr int kStrip = 4;  // output positions per thread step
 
 __global__ void __launch_bounds__(kPolThreads)
 conv_stub_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W, int C,
-                 const float *__restrict__ conv, const float *__restrict__ proj, int J,
-                 double *__restrict__ out, int bulk) {
+                 const float *__restrict__ conv, float *__restrict__ feat, int bulk) {
   extern __shared__ __align__(16) unsigned char sm[];
   float *s_w = reinterpret_cast<float *>(sm);          // (K*K*C, 16): row (ky, kx, c)
   uint8_t *s_obs0 = sm + kK * kK * C * kF * sizeof(float);  // two frame buffers
-  __shared__ float s_red[kPolThreads / 32][kMaxJoints];
   __shared__ uint64_t s_bar[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int oh = (H - kK) / kS + 1, ow = (W - kK) / kS + 1;
@@ -66,9 +66,6 @@ conv_stub_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W, i
       for (int i = tid; i < frame; i += kPolThreads) s_obs[i] = src[i];
       __syncthreads();
     }
-    float pacc[kMaxJoints];
-#pragma unroll
-    for (int j = 0; j < kMaxJoints; j++) pacc[j] = 0.0f;
     // each thread owns strips of kStrip adjacent output positions (same oy):
     // one broadcast load of a weight row feeds kStrip x 16 FMAs
     const int strips_x = (ow + kStrip - 1) / kStrip;
@@ -96,33 +93,65 @@ conv_stub_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W, i
           }
         }
       }
+      // ReLU'd features in (oy, ox, f) order: kStrip x 16 consecutive floats
+      float *fo = feat + env * (int64_t)(oh * ow * kF) + (int64_t)(oy * ow + ox0) * kF;
 #pragma unroll
       for (int i = 0; i < kStrip; i++) {
         if (i >= nx) break;
-        const float *pr = proj + (int64_t)(oy * ow + ox0 + i) * kF * J;
 #pragma unroll
-        for (int f = 0; f < kF; f++) {
-          const float v = acc[i][f] > 0.0f ? acc[i][f] : 0.0f;  // ReLU
+        for (int f = 0; f < kF; f += 4)
+          *reinterpret_cast<float4 *>(fo + i * kF + f) =
+              make_float4(fmaxf(acc[i][f], 0.0f), fmaxf(acc[i][f + 1], 0.0f),
+                          fmaxf(acc[i][f + 2], 0.0f), fmaxf(acc[i][f + 3], 0.0f));
+      }
+    }
+  }
+}
+
+// Projection + tanh: one warp per env; lane l accumulates the features
+// k = l, l + 32, ... in ascending order against tiles of proj staged in
+// shared memory (shared by the CTA's kProjEnvs envs), then a fixed xor tree
+// -- the same arithmetic for a row whatever batch it is in.
+constexpr int kProjEnvs = 8;
+constexpr int kProjTile = 256;  // proj rows per shared-memory tile
+
+__global__ void __launch_bounds__(kProjEnvs * 32)
+conv_proj_kernel(const float *__restrict__ feat, int64_t batch, int K,
+                 const float *__restrict__ proj, int J, double *__restrict__ out) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  float *s_p = reinterpret_cast<float *>(sm);  // kProjTile x J
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t e0 = (int64_t)blockIdx.x * kProjEnvs; e0 < batch;
+       e0 += (int64_t)gridDim.x * kProjEnvs) {
+    const int64_t env = e0 + warp;
+    const float *fr = feat + env * (int64_t)K;
+    float pacc[kMaxJoints];
+#pragma unroll
+    for (int j = 0; j < kMaxJoints; j++) pacc[j] = 0.0f;
+    for (int k0 = 0; k0 < K; k0 += kProjTile) {
+      const int kn = min(kProjTile, K - k0);
+      __syncthreads();  // previous tile no longer read
+      for (int i = tid; i < kn * J; i += kProjEnvs * 32) s_p[i] = __ldg(proj + (int64_t)k0 * J + i);
+      __syncthreads();
+      if (env < batch) {
+        for (int kk = lane; kk < kn; kk += 32) {
+          const float v = __ldg(fr + k0 + kk);
+          const float *pr = s_p + kk * J;
 #pragma unroll
           for (int j = 0; j < kMaxJoints; j++)
-            if (j < J) pacc[j] = __fmaf_rn(v, __ldg(pr + f * J + j), pacc[j]);
+            if (j < J) pacc[j] = __fmaf_rn(v, pr[j], pacc[j]);
         }
       }
     }
-    // fixed-order reduction: xor tree inside the warp, warps in index order
+    if (env < batch) {
 #pragma unroll
-    for (int j = 0; j < kMaxJoints; j++) {
-      if (j >= J) break;
-      float v = pacc[j];
+      for (int j = 0; j < kMaxJoints; j++) {
+        if (j >= J) break;
+        float v = pacc[j];
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) s_red[warp][j] = v;
-    }
-    __syncthreads();
-    if (tid < J) {
-      float v = s_red[0][tid];
-      for (int w = 1; w < kPolThreads / 32; w++) v += s_red[w][tid];
-      out[env * J + tid] = (double)tanhf(v);
+        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == j) out[env * J + j] = (double)tanhf(v);
+      }
     }
   }
 }
@@ -134,8 +163,9 @@ using namespace pxr;
 extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, int32_t height,
                                            int32_t width, int32_t channels, const float *conv,
                                            const float *proj, int32_t n_joints, double *out,
-                                           void *stream) {
-  if (obs == nullptr || conv == nullptr || proj == nullptr || out == nullptr)
+                                           float *workspace, void *stream) {
+  if (obs == nullptr || conv == nullptr || proj == nullptr || out == nullptr ||
+      workspace == nullptr)
     return set_invalid("null pointer");
   if (batch < 0) return set_invalid("batch must be >= 0");
   if (height < kK || width < kK) return set_invalid("observation smaller than the conv kernel");
@@ -146,6 +176,7 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   const int bulk = (frame % 16 == 0) && ((reinterpret_cast<uintptr_t>(obs) & 15) == 0);
   const int smem = kK * kK * channels * kF * (int)sizeof(float) + 2 * ((frame + 15) & ~15);
   if (smem > 200 * 1024) return set_unsupported("observation too large for the policy kernel");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaFuncSetAttribute(conv_stub_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
@@ -154,9 +185,20 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_stub_kernel, kPolThreads, smem);
   if (per_sm < 1) per_sm = 1;
-  const int64_t cap = (int64_t)sms * per_sm;
-  const int grid = (int)(batch < cap ? batch : cap);
-  conv_stub_kernel<<<grid, kPolThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-      obs, batch, height, width, channels, conv, proj, n_joints, out, bulk);
-  return check_launch("conv_stub_kernel");
+  int64_t cap = (int64_t)sms * per_sm;
+  int grid = (int)(batch < cap ? batch : cap);
+  conv_stub_kernel<<<grid, kPolThreads, smem, st>>>(obs, batch, height, width, channels, conv,
+                                                    workspace, bulk);
+  pxr_status s = check_launch("conv_stub_kernel");
+  if (s != PXR_OK) return s;
+  const int K = ((height - kK) / kS + 1) * ((width - kK) / kS + 1) * kF;
+  const int psmem = kProjTile * n_joints * (int)sizeof(float);
+  per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_proj_kernel, kProjEnvs * 32, psmem);
+  if (per_sm < 1) per_sm = 1;
+  cap = (int64_t)sms * per_sm;
+  const int64_t groups = (batch + kProjEnvs - 1) / kProjEnvs;
+  grid = (int)(groups < cap ? groups : cap);
+  conv_proj_kernel<<<grid, kProjEnvs * 32, psmem, st>>>(workspace, batch, K, proj, n_joints, out);
+  return check_launch("conv_proj_kernel");
 }
