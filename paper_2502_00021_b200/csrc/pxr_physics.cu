@@ -46,20 +46,23 @@ struct Model {
   int nl;
 };
 
-// physics.py:166-238 (with the kinematics pass of 144-163 folded in)
+// physics.py:166-238 (with the kinematics pass of 144-163 folded in). The
+// link angles depend on q only, so their cos / sin (ct, st) are computed once
+// per substep by the caller -- the same values the reference recomputes in
+// every pass.
 __device__ void rnea(const Model &m, const double *q, const double *qd, const double *qdd,
-                     double grav, const double *fex, const double *fez, const double *tex,
-                     bool use_ext, double *out) {
-  double theta[kMaxL], omega[kMaxL], alpha[kMaxL], ox[kMaxL], oz[kMaxL], vox[kMaxL],
+                     const double *ct, const double *st, double grav, const double *fex,
+                     const double *fez, const double *tex, bool use_ext, double *out) {
+  double omega[kMaxL], alpha[kMaxL], ox[kMaxL], oz[kMaxL], vox[kMaxL],
       voz[kMaxL], aox[kMaxL], aoz[kMaxL], fx[kMaxL], fz[kMaxL], nq[kMaxL];
   const int nl = m.nl;
-  theta[0] = q[2]; omega[0] = qd[2]; alpha[0] = qdd[2];
+  omega[0] = qd[2]; alpha[0] = qdd[2];
   ox[0] = q[0]; oz[0] = q[1];
   vox[0] = qd[0]; voz[0] = qd[1];
   aox[0] = qdd[0]; aoz[0] = qdd[1];
   for (int i = 1; i < nl; i++) {
     const int p = m.parent[i];
-    const double c = cos(theta[p]), s = sin(theta[p]);
+    const double c = ct[p], s = st[p];
     const double a = m.adist[i];
     ox[i] = ox[p] + a * c;
     oz[i] = oz[p] + a * s;
@@ -67,14 +70,13 @@ __device__ void rnea(const Model &m, const double *q, const double *qd, const do
     voz[i] = voz[p] + omega[p] * a * c;
     aox[i] = aox[p] + alpha[p] * a * (-s) - omega[p] * omega[p] * a * c;
     aoz[i] = aoz[p] + alpha[p] * a * c - omega[p] * omega[p] * a * s;
-    theta[i] = theta[p] + q[3 + i - 1];
     omega[i] = omega[p] + qd[3 + i - 1];
     alpha[i] = alpha[p] + qdd[3 + i - 1];
   }
   for (int i = 0; i < nl; i++) fx[i] = fz[i] = nq[i] = 0.0;
   for (int i = nl - 1; i >= 0; i--) {
     const double h = 0.5 * m.length[i];
-    const double c = cos(theta[i]), s = sin(theta[i]);
+    const double c = ct[i], s = st[i];
     const double acx = aox[i] + alpha[i] * h * (-s) - omega[i] * omega[i] * h * c;
     const double acz = aoz[i] + alpha[i] * h * c - omega[i] * omega[i] * h * s;
     const double gfx = m.mass[i] * acx;
@@ -89,7 +91,7 @@ __device__ void rnea(const Model &m, const double *q, const double *qd, const do
     }
     const int p = m.parent[i];
     if (p >= 0) {
-      const double cp = cos(theta[p]), sp = sin(theta[p]);
+      const double cp = ct[p], sp = st[p];
       const double rx = m.adist[i] * cp, rz = m.adist[i] * sp;
       fx[p] += fx[i];
       fz[p] += fz[i];
@@ -182,25 +184,31 @@ __global__ void physics_step_kernel(StepArgs a) {
     const double x_before = q[0];
     for (int sub = 0; sub < a.substeps; sub++) {
       // kinematics pass (physics.py:144-163)
-      double theta[kMaxL], omega[kMaxL], ox[kMaxL], oz[kMaxL], vox[kMaxL], voz[kMaxL];
-      theta[0] = qb[2]; omega[0] = qdb[2];
+      double theta[kMaxL], ct[kMaxL], st[kMaxL], omega[kMaxL], ox[kMaxL], oz[kMaxL],
+          vox[kMaxL], voz[kMaxL];
+      theta[0] = qb[2];
+      for (int i = 1; i < nl; i++) theta[i] = theta[m.parent[i]] + qb[3 + i - 1];
+      for (int i = 0; i < nl; i++) {
+        ct[i] = cos(theta[i]);
+        st[i] = sin(theta[i]);
+      }
+      omega[0] = qdb[2];
       ox[0] = qb[0]; oz[0] = qb[1];
       vox[0] = qdb[0]; voz[0] = qdb[1];
       for (int i = 1; i < nl; i++) {
         const int p = m.parent[i];
-        const double c = cos(theta[p]), s = sin(theta[p]);
+        const double c = ct[p], s = st[p];
         const double ad = m.adist[i];
         ox[i] = ox[p] + ad * c;
         oz[i] = oz[p] + ad * s;
         vox[i] = vox[p] + omega[p] * ad * (-s);
         voz[i] = voz[p] + omega[p] * ad * c;
-        theta[i] = theta[p] + qb[3 + i - 1];
         omega[i] = omega[p] + qdb[3 + i - 1];
       }
       // ground contact at both capsule ends (physics.py:321-353)
       for (int i = 0; i < nl; i++) fex[i] = fez[i] = tex[i] = 0.0;
       for (int i = 0; i < nl; i++) {
-        const double c = cos(theta[i]), s = sin(theta[i]);
+        const double c = ct[i], s = st[i];
         for (int end = 0; end < 2; end++) {
           double px, pz, vx, vz;
           if (end == 0) {
@@ -238,11 +246,11 @@ __global__ void physics_step_kernel(StepArgs a) {
         t -= JOINT_DAMPING * qdb[3 + j];
         tau[3 + j] = t;
       }
-      rnea(m, qb, qdb, zeros, GRAVITY, fex, fez, tex, true, bias);
+      rnea(m, qb, qdb, zeros, ct, st, GRAVITY, fex, fez, tex, true, bias);
       for (int j = 0; j < nd; j++) unit[j] = 0.0;
       for (int j = active0; j < nd; j++) {
         unit[j] = 1.0;
-        rnea(m, qb, zeros, unit, 0.0, fex, fez, tex, false, col);
+        rnea(m, qb, zeros, unit, ct, st, 0.0, fex, fez, tex, false, col);
         unit[j] = 0.0;
         for (int i = 0; i < nd; i++) M[i * kMaxD + j] = col[i];
       }
