@@ -31,7 +31,7 @@ conv_stub_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W, i
   float *s_w = reinterpret_cast<float *>(sm);          // (K*K*C, 16): row (ky, kx, c)
   uint8_t *s_obs0 = sm + kK * kK * C * kF * sizeof(float);  // two frame buffers
   __shared__ uint64_t s_bar[2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int oh = (H - kK) / kS + 1, ow = (W - kK) / kS + 1;
   const int nw = kK * kK * C * kF;
   const int frame = H * W * C;
