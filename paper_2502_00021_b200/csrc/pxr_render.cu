@@ -141,7 +141,6 @@ struct RenderParams {
   int frag_limit;  // fragment list limit (kFragCap; test override)
   int frame_bytes, use_bulk, vframe_bytes, vframe_bulk;
   uint32_t wmagic;  // ceil(2^32 / W): flat pixel index -> row
-  uint32_t gmagic;  // ceil(2^32 / (W / 4)): 4-pixel group -> row (W % 4 == 0)
   int depth_vec;    // out_depth groups of 4 pixels are 16-byte aligned
   int band_h;       // rows per band: a frame is rendered in bands that fit shared memory
 };
@@ -603,7 +602,7 @@ render_step_kernel(const RenderParams p) {
     if (p.draw_floor && p.floor_sep) {
       // separable floor rays: t = -ez / dz and floor(wy) depend on the row
       // only (render.py:321-334), computed once per row by the last threads
-      // (the ones with a single vertex below)
+      // (those with no or one vertex below)
       for (int y = kThreads - 1 - tid; y < p.H; y += kThreads) {
         const double dy = s_floor[p.W + y], dz = s_floor[p.W + p.H + y];
         double t = 0.0;
@@ -926,7 +925,7 @@ render_step_kernel(const RenderParams p) {
         // the exact test on them, so the f64 work runs on full warps even
         // though most rows of the thin triangles hold no pixel centre.
         const int n_chunks = (n_rows + 31) >> 5;
-        if (warp == kWarps - 1 && !prepared) {  // joins the chunk queue afterwards
+        if (warp == kWarps - 1 && !prepared) {  // joins the chunks afterwards
           prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
                       lane);
           prepared = true;
@@ -1075,7 +1074,7 @@ render_step_kernel(const RenderParams p) {
       if (warp == kWarps - 1 && !prepared)  // env without live triangles
         prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es, lane);
 
-      // ---- phase 5: depth output (debug / _render_frame parity only) ------
+      // ---- depth output (debug / _render_frame parity only) ---------------
       if (p.out_depth != nullptr) {
         float *dd = p.out_depth + (int64_t)env * fpx + (int64_t)y0 * p.W;
         if (p.depth_vec)
@@ -1085,7 +1084,7 @@ render_step_kernel(const RenderParams p) {
           dd[i] = s_depth[i];
       }
 
-      // ---- phase 6: frame -> HBM (one TMA bulk store) --------------------
+      // ---- phase 5: frame -> HBM (one TMA bulk store) --------------------
       uint8_t *gout = p.out + (int64_t)env * p.frame_bytes + (int64_t)y0 * p.W * chans;
       const int band_bytes = npx * chans;
       if (p.use_bulk) {  // host: every band's size and offset are multiples of 16
@@ -1268,7 +1267,6 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   if (npx64 > (1 << 20) || height > 4096 || width > 4096)
     return set_unsupported("frame too large");
   p.wmagic = (uint32_t)((0x100000000ull + (uint64_t)width - 1) / (uint64_t)width);
-  p.gmagic = (uint32_t)((0x100000000ull + (uint64_t)(width / 4) - 1) / (uint64_t)(width / 4));
   p.depth_vec = out_depth != nullptr && (npx64 % 4 == 0) &&
                 ((reinterpret_cast<uintptr_t>(out_depth) & 15) == 0);
   p.frame_bytes = (int)(npx64 * C);
