@@ -3,14 +3,15 @@
 // obs / 255, ReLU, linear projection of the (oy, ox, f)-ordered features,
 // tanh.
 //
-// Two kernels: the convolution (one CTA per env, frames by double-buffered
-// TMA bulk copies, each thread a strip of 4 output positions x 16 filters)
-// writes ReLU'd features to a workspace; the projection (one warp per env,
-// proj tiles in shared memory shared by 8 envs) reduces them in a fixed
-// order. A batch row therefore never depends on the batch it is in
-// (reference tests/test_bench.py:92-98). f32 arithmetic like
-// the reference's f32 BLAS path; accuracy is checked against a float64
-// evaluation (<= 1e-5, tests/test_bench.py:56-68).
+// Two kernels. The convolution runs on the 5th-generation tensor cores
+// (tcgen05.mma kind::f16, accumulator in TMEM, frames by double-buffered TMA
+// bulk copies): obs bytes are exact in bf16 and the f32 weights are split
+// into three bf16 parts, so the products are exact and only the f32
+// accumulation rounds. It writes the ReLU'd features to a workspace; the
+// projection (one warp per env, proj tiles in shared memory shared by 8
+// envs) reduces them in a fixed order. Each batch row is computed by the
+// same instructions in the same order whatever batch it is in (reference
+// tests/test_bench.py:92-98), within 1e-5 of a float64 evaluation.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -19,99 +20,208 @@
 
 namespace pxr {
 
-constexpr int kPolThreads = 128;
 constexpr int kK = 8, kS = 4, kF = 16;
 constexpr int kMaxJoints = 32;
-constexpr int kStrip = 4;  // output positions per thread step
 
-__global__ void __launch_bounds__(kPolThreads)
-conv_stub_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W, int C,
-                 const float *__restrict__ conv, float *__restrict__ feat, int bulk) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  float *s_w = reinterpret_cast<float *>(sm);          // (K*K*C, 16): row (ky, kx, c)
-  uint8_t *s_obs0 = sm + kK * kK * C * kF * sizeof(float);  // two frame buffers
-  __shared__ uint64_t s_bar[2];
-  const int tid = threadIdx.x;
-  const int oh = (H - kK) / kS + 1, ow = (W - kK) / kS + 1;
-  const int nw = kK * kK * C * kF;
+// Projection + tanh: one warp per env; lane l accumulates the features
+// k = l, l + 32, ... in ascending order against tiles of proj staged in
+// shared memory (shared by the CTA's kProjEnvs envs), then a fixed xor tree
+// -- the same arithmetic for a row whatever batch it is in.
+// ---- tensor-core convolution (tcgen05, BF16 in, F32 accumulate in TMEM) ----
+// Per env and per tile of 128 output positions: D[128 x 48] = A[128 x K] *
+// B[48 x K]^T with K = 64 C in steps of 16. A is the im2col of the raw obs
+// bytes (0..255, exact in bf16); B holds the f32 weights split into three
+// bf16 parts w = w1 + w2 + w3 (24 significant bits), columns n = split*16 + f.
+// The products are exact and accumulate in f32; the epilogue adds the three
+// splits in a fixed order, scales by float32(1/255) and applies the ReLU.
+// Operands use the K-major no-swizzle canonical layout: 8-row x 16-byte core
+// matrices, LBO = 128 B between the two 8-element K halves, SBO = 256 B
+// between 8-row groups. One thread issues the MMAs; tcgen05.commit arrives
+// on an mbarrier the CTA waits on before reading TMEM.
+constexpr int kTcThreads = 256;
+constexpr int kTcM = 128, kTcN = 48;
+
+__device__ __forceinline__ uint32_t tc_off(int row, int k, int step_bytes) {
+  return (uint32_t)((k >> 4) * step_bytes + (row >> 3) * 256 + ((k >> 3) & 1) * 128 +
+                    (row & 7) * 16 + (k & 7) * 2);
+}
+
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
+}
+
+__device__ __forceinline__ uint32_t bf16x2_of_bytes(uint32_t b0, uint32_t b1) {
+  const float f0 = __int_as_float(0x4B000000 | b0) - 8388608.0f;  // exact integers
+  const float f1 = __int_as_float(0x4B000000 | b1) - 8388608.0f;
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(f1), "f"(f0));
+  return r;
+}
+
+__device__ __forceinline__ uint16_t bf16_bits(float x) {
+  uint16_t r;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float bf16_val(uint16_t h) {
+  return __uint_as_float((uint32_t)h << 16);
+}
+
+__global__ void __launch_bounds__(kTcThreads)
+conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W, int C,
+                    const float *__restrict__ conv, float *__restrict__ feat, int bulk) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const int K = kK * kK * C;           // 64 C, a multiple of 16
+  const int a_step = (kTcM / 8) * 256;  // bytes per 16-wide K step of A
+  const int b_step = (kTcN / 8) * 256;
+  unsigned char *s_a = sm;
+  unsigned char *s_b = s_a + (K / 16) * a_step;
+  uint8_t *s_obs0 = s_b + (K / 16) * b_step;
   const int frame = H * W * C;
-  const float inv = 1.0f / 255.0f;  // float32(1/255), bench.py:101
   const int fstride = (frame + 15) & ~15;
-  for (int i = tid; i < nw; i += kPolThreads) s_w[i] = conv[i];
-  // frames arrive by TMA bulk copy, the next env's while this one is
-  // convolved (bulk: frame size and base 16-byte aligned), else byte loads
-  if (bulk && tid == 0) {
+  __shared__ uint64_t s_bar[3];  // frame buffers 0 / 1, MMA completion
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int oh = (H - kK) / kS + 1, ow = (W - kK) / kS + 1, n_pos = oh * ow;
+  const float inv = 1.0f / 255.0f;  // float32(1/255), bench.py:101
+
+  // B: the three bf16 splits of every weight, K-major
+  for (int i = tid; i < K * kF; i += kTcThreads) {
+    const int k = i / kF, f = i - k * kF;
+    const float w = conv[i];
+    const uint16_t h1 = bf16_bits(w);
+    const float r1 = w - bf16_val(h1);
+    const uint16_t h2 = bf16_bits(r1);
+    const uint16_t h3 = bf16_bits(r1 - bf16_val(h2));
+    *reinterpret_cast<uint16_t *>(s_b + tc_off(f, k, b_step)) = h1;
+    *reinterpret_cast<uint16_t *>(s_b + tc_off(16 + f, k, b_step)) = h2;
+    *reinterpret_cast<uint16_t *>(s_b + tc_off(32 + f, k, b_step)) = h3;
+  }
+  if (warp == 0) {  // 64 TMEM columns hold the 128 x 48 f32 accumulator
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
+    mbar_init(&s_bar[2], 1);
     fence_mbar_init();
-    if (blockIdx.x < batch) {
+    if (bulk && blockIdx.x < batch) {
       mbar_arrive_expect_tx(&s_bar[0], (uint32_t)frame);
       bulk_load_g2s(s_obs0, obs + (int64_t)blockIdx.x * frame, (uint32_t)frame, &s_bar[0]);
     }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = s_tmem;
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
+                         ((uint32_t)(kTcM >> 4) << 24);
+  const uint32_t a_base = (uint32_t)__cvta_generic_to_shared(s_a);
+  const uint32_t b_base = (uint32_t)__cvta_generic_to_shared(s_b);
+  uint32_t mma_phase = 0;
   int it = 0;
   for (int64_t env = blockIdx.x; env < batch; env += gridDim.x, it++) {
-    __syncthreads();  // weights loaded / the other buffer no longer read
+    __syncthreads();  // the other frame buffer is no longer read
     uint8_t *s_obs = s_obs0 + (it & 1) * fstride;
     if (bulk) {
       const int64_t nxt = env + gridDim.x;
       if (tid == 0 && nxt < batch) {
         uint64_t *bar = &s_bar[(it + 1) & 1];
         mbar_arrive_expect_tx(bar, (uint32_t)frame);
-        bulk_load_g2s(s_obs0 + ((it + 1) & 1) * fstride, obs + nxt * frame, (uint32_t)frame, bar);
+        bulk_load_g2s(s_obs0 + ((it + 1) & 1) * fstride, obs + nxt * frame, (uint32_t)frame,
+                      bar);
       }
       mbar_wait_parity(&s_bar[it & 1], (uint32_t)((it >> 1) & 1));
     } else {
       const uint8_t *src = obs + env * (int64_t)frame;
-      for (int i = tid; i < frame; i += kPolThreads) s_obs[i] = src[i];
+      for (int i = tid; i < frame; i += kTcThreads) s_obs[i] = src[i];
       __syncthreads();
     }
-    // each thread owns strips of kStrip adjacent output positions (same oy):
-    // one broadcast load of a weight row feeds kStrip x 16 FMAs
-    const int strips_x = (ow + kStrip - 1) / kStrip;
-    for (int st = tid; st < oh * strips_x; st += kPolThreads) {
-      const int oy = st / strips_x, ox0 = (st - oy * strips_x) * kStrip;
-      const int nx = min(kStrip, ow - ox0);
-      float acc[kStrip][kF];
-#pragma unroll
-      for (int i = 0; i < kStrip; i++)
-#pragma unroll
-        for (int f = 0; f < kF; f++) acc[i][f] = 0.0f;
-      for (int ky = 0; ky < kK; ky++) {
-        const uint8_t *row = s_obs + ((oy * kS + ky) * W + ox0 * kS) * C;
-        for (int kc = 0; kc < kK * C; kc++) {  // (kx, c) in memory order
-          const float4 *w4 = reinterpret_cast<const float4 *>(s_w + (ky * kK * C + kc) * kF);
-          const float4 wa = w4[0], wb = w4[1], wc = w4[2], wd = w4[3];  // broadcast
-          const float w[kF] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w,
-                               wc.x, wc.y, wc.z, wc.w, wd.x, wd.y, wd.z, wd.w};
-#pragma unroll
-          for (int i = 0; i < kStrip; i++) {
-            // positions past the edge read in-bounds pixels and are dropped
-            const float x = (float)row[(i < nx ? i : 0) * kS * C + kc] * inv;
-#pragma unroll
-            for (int f = 0; f < kF; f++) acc[i][f] = __fmaf_rn(x, w[f], acc[i][f]);
+    float *fe = feat + env * (int64_t)(n_pos * kF);
+    for (int m0 = 0; m0 < n_pos; m0 += kTcM) {
+      // A: im2col rows of this tile; item (row, ky) = 8 C consecutive bytes
+      for (int item = tid; item < kTcM * kK; item += kTcThreads) {
+        const int row = item >> 3, ky = item & 7, pos = m0 + row;
+        if (pos >= n_pos) continue;  // rows past the end are computed and dropped
+        const int oy = pos / ow, ox = pos - oy * ow;
+        const int boff = ((oy * kS + ky) * W + ox * kS) * C;
+        const uint8_t *src = s_obs + boff;
+        for (int ch = 0; ch < C; ch++) {  // 8-element K chunks
+          uint32_t lo, hi;
+          if (((boff + 8 * ch) & 3) == 0) {  // two aligned words
+            lo = *reinterpret_cast<const uint32_t *>(src + 8 * ch);
+            hi = *reinterpret_cast<const uint32_t *>(src + 8 * ch + 4);
+          } else {
+            const uint8_t *b8 = src + 8 * ch;
+            lo = b8[0] | (b8[1] << 8) | (b8[2] << 16) | ((uint32_t)b8[3] << 24);
+            hi = b8[4] | (b8[5] << 8) | (b8[6] << 16) | ((uint32_t)b8[7] << 24);
           }
+          uint4 v;
+          v.x = bf16x2_of_bytes(lo & 0xffu, (lo >> 8) & 0xffu);
+          v.y = bf16x2_of_bytes((lo >> 16) & 0xffu, lo >> 24);
+          v.z = bf16x2_of_bytes(hi & 0xffu, (hi >> 8) & 0xffu);
+          v.w = bf16x2_of_bytes((hi >> 16) & 0xffu, hi >> 24);
+          *reinterpret_cast<uint4 *>(s_a + tc_off(row, ky * 8 * C + 8 * ch, a_step)) = v;
         }
       }
-      // ReLU'd features in (oy, ox, f) order: kStrip x 16 consecutive floats
-      float *fo = feat + env * (int64_t)(oh * ow * kF) + (int64_t)(oy * ow + ox0) * kF;
-#pragma unroll
-      for (int i = 0; i < kStrip; i++) {
-        if (i >= nx) break;
-#pragma unroll
-        for (int f = 0; f < kF; f += 4)
-          *reinterpret_cast<float4 *>(fo + i * kF + f) =
-              make_float4(fmaxf(acc[i][f], 0.0f), fmaxf(acc[i][f + 1], 0.0f),
-                          fmaxf(acc[i][f + 2], 0.0f), fmaxf(acc[i][f + 3], 0.0f));
+      fence_proxy_async_smem();  // generic-proxy writes -> tensor-core (async) reads
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (tid == 0) {
+        for (int s = 0; s < K / 16; s++) {
+          const uint64_t da = tc_desc(a_base + s * a_step), db = tc_desc(b_base + s * b_step);
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(idesc), "r"(s));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     ::"r"((uint32_t)__cvta_generic_to_shared(&s_bar[2])));
       }
+      mbar_wait_parity(&s_bar[2], mma_phase);
+      mma_phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (its rows) and
+      // filters 8 (w / 4) .. +7 of each split
+      const int q = warp & 3, fh = (warp >> 2) * 8;
+      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16);
+      uint32_t d[3][8];
+#pragma unroll
+      for (int sp = 0; sp < 3; sp++)
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+            : "=r"(d[sp][0]), "=r"(d[sp][1]), "=r"(d[sp][2]), "=r"(d[sp][3]), "=r"(d[sp][4]),
+              "=r"(d[sp][5]), "=r"(d[sp][6]), "=r"(d[sp][7])
+            : "r"(ta + (uint32_t)(sp * 16 + fh)));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      const int pos = m0 + 32 * q + lane;
+      if (pos < n_pos) {
+        float o[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const float v = (__uint_as_float(d[0][i]) + __uint_as_float(d[1][i]) +
+                           __uint_as_float(d[2][i])) * inv;
+          o[i] = v > 0.0f ? v : 0.0f;  // ReLU
+        }
+        float4 *dst = reinterpret_cast<float4 *>(fe + pos * kF + fh);
+        dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+        dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();  // TMEM and A are reused by the next tile
+      asm volatile("tcgen05.fence::after_thread_sync;");
     }
   }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
 }
 
-// Projection + tanh: one warp per env; lane l accumulates the features
-// k = l, l + 32, ... in ascending order against tiles of proj staged in
-// shared memory (shared by the CTA's kProjEnvs envs), then a fixed xor tree
-// -- the same arithmetic for a row whatever batch it is in.
 constexpr int kProjEnvs = 8;
 constexpr int kProjTile = 256;  // proj rows per shared-memory tile
 
@@ -174,22 +284,33 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   if (batch == 0) return PXR_OK;
   const int frame = height * width * channels;
   const int bulk = (frame % 16 == 0) && ((reinterpret_cast<uintptr_t>(obs) & 15) == 0);
-  const int smem = kK * kK * channels * kF * (int)sizeof(float) + 2 * ((frame + 15) & ~15);
-  if (smem > 200 * 1024) return set_unsupported("observation too large for the policy kernel");
+  const int Kc = kK * kK * channels;
+  const int smem = (Kc / 16) * ((kTcM / 8) * 256) + (Kc / 16) * ((kTcN / 8) * 256) +
+                   2 * ((frame + 15) & ~15);
+  if (smem > 220 * 1024) return set_unsupported("observation too large for the policy kernel");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaFuncSetAttribute(conv_stub_kernel,
+  cudaError_t e = cudaFuncSetAttribute(conv_feat_tc_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
+  // the full shared-memory carveout, so two CTAs (frames + operands) share an SM
+  e = cudaFuncSetAttribute(conv_feat_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           100);
   if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_stub_kernel, kPolThreads, smem);
+  // CTAs per SM from the shared memory per SM (the occupancy query does not
+  // see the carveout preference set above)
+  int smem_sm = 0;
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  per_sm = smem_sm / (smem + 2048);
+  if (per_sm > 2048 / kTcThreads) per_sm = 2048 / kTcThreads;
   if (per_sm < 1) per_sm = 1;
   int64_t cap = (int64_t)sms * per_sm;
   int grid = (int)(batch < cap ? batch : cap);
-  conv_stub_kernel<<<grid, kPolThreads, smem, st>>>(obs, batch, height, width, channels, conv,
-                                                    workspace, bulk);
-  pxr_status s = check_launch("conv_stub_kernel");
+  conv_feat_tc_kernel<<<grid, kTcThreads, smem, st>>>(obs, batch, height, width, channels, conv,
+                                                      workspace, bulk);
+  pxr_status s = check_launch("conv_feat_tc_kernel");
   if (s != PXR_OK) return s;
   const int K = ((height - kK) / kS + 1) * ((width - kK) / kS + 1) * kF;
   const int psmem = kProjTile * n_joints * (int)sizeof(float);
