@@ -213,12 +213,14 @@ def robot_cams(poses: np.ndarray, offset=CAM_OFFSET, fov=0.9, near=0.1, far=50.0
 
 
 def render_robot_batch(geom, poses: np.ndarray, width: int, height: int,
-                       floor_in_background: bool, threads: int = 1):
+                       floor_in_background: bool, threads: int = 1, offset=CAM_OFFSET,
+                       fov: float = 0.9, near: float = 0.1, far: float = 50.0):
     """render.py:594-623 on the C oracle. ``geom`` needs base_verts,
-    vert_link, triangles, tri_colors (the RobotGeometry layout)."""
+    vert_link, triangles, tri_colors (the RobotGeometry layout); the camera
+    follows CameraConfig(offset, vertical_fov, near, far)."""
     poses = np.ascontiguousarray(poses, dtype=np.float64)
     batch, n_links, _ = poses.shape
-    cams = robot_cams(poses)
+    cams = robot_cams(poses, offset=offset, fov=fov, near=near, far=far)
     poses32 = np.ascontiguousarray(poses.astype(np.float32))
     bv = np.ascontiguousarray(geom.base_verts, dtype=np.float32)
     vl = np.ascontiguousarray(geom.vert_link, dtype=np.int32)
