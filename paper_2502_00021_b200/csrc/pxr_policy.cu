@@ -72,7 +72,7 @@ __device__ __forceinline__ float bf16_val(uint16_t h) {
 __global__ void __launch_bounds__(kTcThreads)
 conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W, int C,
                     const float *__restrict__ conv, float *__restrict__ feat, int bulk) {
-  extern __shared__ __align__(1024) unsigned char sm[];
+  extern __shared__ __align__(16) unsigned char sm[];
   const int K = kK * kK * C;           // 64 C, a multiple of 16
   const int a_step = (kTcM / 8) * 256;  // bytes per 16-wide K step of A
   const int b_step = (kTcN / 8) * 256;
