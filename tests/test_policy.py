@@ -104,6 +104,29 @@ class TestConvStubGPU:
         assert torch.equal(B.conv_stub_forward(stub, obs[10:30]), full[10:30])
         assert bool((full.abs() <= 1.0).all())
 
+    def test_matches_torch_conv2d_formulation(self, B, torch):
+        """Weight-layout parity with the PyTorch formulation of the stub
+        (SURVEY 8(f) row 3): conv weight (ky, kx, c, f) -> torch (f, c, ky,
+        kx), features flattened in (oy, ox, f) order, f32 without TF32."""
+        import torch.nn.functional as Fn
+
+        stub = B.ConvStub.create(84, 84, 3, 17, seed=5)
+        obs = torch.randint(0, 256, (64, 84, 84, 3), dtype=torch.uint8, device="cuda")
+        w = torch.from_numpy(stub.conv).cuda().reshape(8, 8, 3, 16).permute(3, 2, 0, 1)
+        p = torch.from_numpy(stub.proj).cuda()
+        with torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+            prev = torch.backends.cuda.matmul.allow_tf32
+            torch.backends.cuda.matmul.allow_tf32 = False
+            try:
+                x = obs.permute(0, 3, 1, 2).float() * torch.tensor(1.0 / 255.0,
+                                                                   dtype=torch.float32)
+                feat = torch.relu(Fn.conv2d(x, w, stride=4)).permute(0, 2, 3, 1).reshape(64, -1)
+                want = torch.tanh(feat @ p).double()
+            finally:
+                torch.backends.cuda.matmul.allow_tf32 = prev
+        got = B.conv_stub_forward(stub, obs)
+        assert float((got - want).abs().max()) < 1e-5
+
     def test_zero_weights_and_shape_errors(self, B):
         stub = B.ConvStub.create(32, 32, 3, 4, seed=0)
         zero = dataclasses.replace(stub, conv=np.zeros_like(stub.conv),
