@@ -785,19 +785,13 @@ render_step_kernel(const RenderParams p) {
           s_scan[kWarps + warp] = wr;
         }
         __syncthreads();  // (also publishes s_rows and the background)
-        if (warp == 0) {
-          const int v = lane < kWarps ? s_scan[lane] : 0;
-          const int u = lane < kWarps ? s_scan[kWarps + lane] : 0;
-          const int vi = warp_incl_scan(v, lane), ui = warp_incl_scan(u, lane);
-          if (lane < kWarps) {
-            s_scan[lane] = vi - v;
-            s_scan[kWarps + lane] = ui - u;
-          }
-          if (lane == kWarps - 1) es.n_live = vi;
-        }
-        __syncthreads();
-        int li = s_scan[warp] + wl - my_live;
-        uint32_t racc = (uint32_t)(s_scan[kWarps + warp] + wr - my_rows);
+        // every warp scans the warp totals itself (no second barrier)
+        const int v = lane < kWarps ? s_scan[lane] : 0;
+        const int u = lane < kWarps ? s_scan[kWarps + lane] : 0;
+        const int vi = warp_incl_scan(v, lane), ui = warp_incl_scan(u, lane);
+        if (warp == 0 && lane == kWarps - 1) es.n_live = vi;
+        int li = __shfl_sync(kFull, vi - v, warp) + wl - my_live;
+        uint32_t racc = (uint32_t)(__shfl_sync(kFull, ui - u, warp) + wr - my_rows);
         for (int t = t0; t < t1; t++) {
           const int r = s_rows[t];
           if (r != 0) {
