@@ -1062,7 +1062,9 @@ render_step_kernel(const RenderParams p) {
           if (r1 < n_live)
             for (int i = tid; i < npx; i += kThreads) s_wkey[i] = 0u;
         }
-        __syncthreads();
+        // the next round reuses records and keys; after the last one the
+        // frame store's barrier orders the paint
+        if (r1 < n_live) __syncthreads();
         r0 = r1;
       }
       if (warp == kWarps - 1 && !prepared)  // env without live triangles
