@@ -99,6 +99,9 @@ typedef struct pxr_step_keys {
 /* ------------------------------------------------------------------ */
 
 int32_t pxr_abi_version(void);
+/* 1 for the checked build (libpxr_checked.so: device bounds / invariant
+ * checks compiled in, a failed check traps the launch), else 0. */
+int32_t pxr_build_checked(void);
 const char *pxr_status_string(pxr_status s);
 /* Last CUDA error string seen by a failing call (thread-local). */
 const char *pxr_last_error(void);

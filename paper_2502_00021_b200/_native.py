@@ -27,7 +27,7 @@ MODES = {"none": MODE_NONE, "color": MODE_COLOR, "video": MODE_VIDEO}
 
 # Every symbol include/pxr.h declares (tests check the .so exports them all).
 EXPORTED = (
-    "pxr_abi_version", "pxr_status_string", "pxr_last_error", "pxr_floor_rays",
+    "pxr_abi_version", "pxr_build_checked", "pxr_status_string", "pxr_last_error", "pxr_floor_rays",
     "pxr_render_step", "pxr_advance_distractors", "pxr_init_distractors",
     "pxr_apply_color", "pxr_apply_video", "pxr_grayscale", "pxr_threefry2x64",
     "pxr_sincosf", "pxr_pose_source", "pxr_forward_kinematics", "pxr_div_check",
@@ -113,6 +113,8 @@ def lib() -> ctypes.CDLL:
     P = ctypes.POINTER
     L.pxr_abi_version.restype = _i32
     L.pxr_abi_version.argtypes = []
+    L.pxr_build_checked.restype = _i32
+    L.pxr_build_checked.argtypes = []
     L.pxr_status_string.restype = ctypes.c_char_p
     L.pxr_status_string.argtypes = [_i32]
     L.pxr_last_error.restype = ctypes.c_char_p

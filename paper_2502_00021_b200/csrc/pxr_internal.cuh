@@ -6,6 +6,26 @@
 
 #include "../../include/pxr.h"
 
+// PXR_DCHECK: bounds / invariant checks of the kernels, compiled in only for
+// the checked build (libpxr_checked.so, -DPXR_CHECKED; make checked). A
+// failed check prints the condition and traps, so the launch fails loudly;
+// tests/test_gpu_checked.py runs the fuzz and overflow cases through it.
+#ifdef PXR_CHECKED
+#include <cstdio>
+#define PXR_DCHECK(cond)                                                            \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      printf("PXR_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x, #cond);                             \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define PXR_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace pxr {
 
 void set_last_error(const char *msg);

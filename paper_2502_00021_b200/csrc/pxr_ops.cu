@@ -232,6 +232,14 @@ using namespace pxr;
 
 extern "C" int32_t pxr_abi_version(void) { return PXR_ABI_VERSION; }
 
+extern "C" int32_t pxr_build_checked(void) {
+#ifdef PXR_CHECKED
+  return 1;
+#else
+  return 0;
+#endif
+}
+
 extern "C" const char *pxr_status_string(pxr_status s) {
   switch (s) {
     case PXR_OK: return "ok";

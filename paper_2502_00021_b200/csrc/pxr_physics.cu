@@ -166,6 +166,10 @@ __global__ void physics_step_kernel(StepArgs a) {
   const Model &m = a.m;
   const int nl = m.nl, nd = nl + 2, nj = nd - 3;
   const int active0 = a.fixed_root ? 3 : 0;
+  PXR_DCHECK(nl >= 1 && nl <= kMaxL && nd <= kMaxD && m.parent[0] < 0);
+#ifdef PXR_CHECKED
+  for (int i = 1; i < nl; i++) PXR_DCHECK(m.parent[i] >= 0 && m.parent[i] < i);
+#endif
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < a.batch;
        b += (int64_t)gridDim.x * blockDim.x) {
     double qb[kMaxD], qdb[kMaxD], q0[kMaxD], tau[kMaxD], bias[kMaxD], col[kMaxD], rhs[kMaxD],

@@ -95,6 +95,7 @@ conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W
     const float r1 = w - bf16_val(h1);
     const uint16_t h2 = bf16_bits(r1);
     const uint16_t h3 = bf16_bits(r1 - bf16_val(h2));
+    PXR_DCHECK(tc_off(32 + f, k, b_step) + 2u <= (uint32_t)((K / 16) * b_step));
     *reinterpret_cast<uint16_t *>(s_b + tc_off(f, k, b_step)) = h1;
     *reinterpret_cast<uint16_t *>(s_b + tc_off(16 + f, k, b_step)) = h2;
     *reinterpret_cast<uint16_t *>(s_b + tc_off(32 + f, k, b_step)) = h3;
@@ -118,6 +119,7 @@ conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = s_tmem;
+  PXR_DCHECK((tmem & 0xFFFFu) + 64u <= 512u);
   const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
                          ((uint32_t)(kTcM >> 4) << 24);
   const uint32_t a_base = (uint32_t)__cvta_generic_to_shared(s_a);
@@ -149,6 +151,7 @@ conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W
         if (pos >= n_pos) continue;  // rows past the end are computed and dropped
         const int oy = pos / ow, ox = pos - oy * ow;
         const int boff = ((oy * kS + ky) * W + ox * kS) * C;
+        PXR_DCHECK(oy * kS + ky < H && ox * kS + kK <= W && boff + 8 * C <= frame);
         const uint8_t *src = s_obs + boff;
         for (int ch = 0; ch < C; ch++) {  // 8-element K chunks
           uint32_t lo, hi;
@@ -165,6 +168,7 @@ conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W
           v.y = bf16x2_of_bytes((lo >> 16) & 0xffu, lo >> 24);
           v.z = bf16x2_of_bytes(hi & 0xffu, (hi >> 8) & 0xffu);
           v.w = bf16x2_of_bytes((hi >> 16) & 0xffu, hi >> 24);
+          PXR_DCHECK(tc_off(row, ky * 8 * C + 8 * ch, a_step) + 16u <= (uint32_t)((K / 16) * a_step));
           *reinterpret_cast<uint4 *>(s_a + tc_off(row, ky * 8 * C + 8 * ch, a_step)) = v;
         }
       }
@@ -235,6 +239,7 @@ conv_proj_kernel(const float *__restrict__ feat, int64_t batch, int K,
        e0 += (int64_t)gridDim.x * kProjEnvs) {
     const int64_t env = e0 + warp;
     const float *fr = feat + env * (int64_t)K;
+    PXR_DCHECK(J >= 1 && J <= kMaxJoints);
     float pacc[kMaxJoints];
 #pragma unroll
     for (int j = 0; j < kMaxJoints; j++) pacc[j] = 0.0f;

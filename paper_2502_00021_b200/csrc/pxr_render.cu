@@ -127,7 +127,7 @@ struct RenderParams {
   const uint8_t *frames;
   const int64_t *starts;
   const int64_t *counts;
-  int64_t n_videos;
+  int64_t n_videos, n_frames;
   int Hv, Wv;
   int advance;
   uint64_t key_hi, key_lo, env_offset, logical_batch;
@@ -246,7 +246,10 @@ __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t
       p.frame_cursor[env] = cur;
       p.direction[env] = (int8_t)dir;
     }
+    PXR_DCHECK(vid >= 0 && vid < p.n_videos);
+    PXR_DCHECK(cur >= 0 && cur < p.counts[vid]);
     out.frame_idx = p.starts[vid] + cur;
+    PXR_DCHECK(out.frame_idx >= 0 && out.frame_idx < p.n_frames);
   }
 }
 
@@ -342,6 +345,7 @@ __device__ __forceinline__ void prepare_env(const RenderParams &p, int64_t env, 
 }
 
 __device__ __forceinline__ float3 world_vertex(const RenderParams &p, const float4 *s_link, int v) {
+  PXR_DCHECK(__ldg(p.vert_link + v) >= 0 && __ldg(p.vert_link + v) < p.nl);
   const float4 lk = s_link[__ldg(p.vert_link + v)];
   const float bx = __ldg(p.base_verts + 3 * v + 0);
   const float by = __ldg(p.base_verts + 3 * v + 1);
@@ -476,6 +480,13 @@ render_step_kernel(const RenderParams p) {
   __shared__ DistSlot s_dist[32];
   __shared__ int s_scan[2 * kWarps];
   const SmemLayout L = smem_layout(p);
+#ifdef PXR_CHECKED
+  {
+    uint32_t dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    PXR_DCHECK((uint32_t)L.total <= dyn);
+  }
+#endif
   float4 *s_link = reinterpret_cast<float4 *>(smem + L.link);
   double *s_floor = reinterpret_cast<double *>(smem + L.floor);  // dx[W], dy[H], dz[H]
   double *s_ft = s_floor + p.W + 2 * p.H;                          // per-row floor t
@@ -591,6 +602,7 @@ render_step_kernel(const RenderParams p) {
     const int cb = local_env & 1;
     const float4 *s_link_cur = s_link + cb * p.nl;
     if (tid == 0 && p.mode == PXR_MODE_VIDEO && p.vframe_bulk) {
+      PXR_DCHECK(es.frame_idx[cb] >= 0 && es.frame_idx[cb] < p.n_frames);
       mbar_arrive_expect_tx(&es.vbar, (uint32_t)p.vframe_bytes);
       bulk_load_g2s(s_vframe, p.frames + es.frame_idx[cb] * p.vframe_bytes,
                     (uint32_t)p.vframe_bytes, &es.vbar);
@@ -666,6 +678,7 @@ render_step_kernel(const RenderParams p) {
       }
       // a pixel's final colour: colour distractor, then grayscale
       auto emit = [&](uint32_t pix, uint32_t rgb) {
+        PXR_DCHECK(pix < (uint32_t)npx);
         if (p.mode == PXR_MODE_COLOR) rgb = __vsubus4(__vaddus4(rgb, bpos), bneg);
         if (p.gray)
           s_gray[pix] = (uint8_t)((299u * (rgb & 0xffu) + 587u * ((rgb >> 8) & 0xffu) +
@@ -698,6 +711,8 @@ render_step_kernel(const RenderParams p) {
           n1 = __ldg(p.tris + 3 * t + 4);
           n2 = __ldg(p.tris + 3 * t + 5);
         }
+        PXR_DCHECK(i0 >= 0 && i0 < p.nv && i1 >= 0 && i1 < p.nv && i2 >= 0 && i2 < p.nv);
+        PXR_DCHECK(rows <= 0xFFFFu);
         const float z0 = s_vz[i0], z1 = s_vz[i1], z2 = s_vz[i2];
         if (!(z0 < near_ || z1 < near_ || z2 < near_) && !(z0 > far_ && z1 > far_ && z2 > far_)) {
           const float2 a = s_vxy32[i0], b = s_vxy32[i1], c = s_vxy32[i2];
@@ -741,6 +756,10 @@ render_step_kernel(const RenderParams p) {
               reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y0 + yb]) + pl.x;
           const uint32_t *w0 = src + (pl.y >> 16), *w1 = src + (pl.z >> 16),
                          *w2 = src + (pl.w >> 16);
+          PXR_DCHECK(4u * (uint32_t)(w0 + 1 - reinterpret_cast<const uint32_t *>(s_vframe)) + 4u <=
+                     (uint32_t)p.vframe_bytes + 32u);
+          PXR_DCHECK(4u * (uint32_t)(w2 + 1 - reinterpret_cast<const uint32_t *>(s_vframe)) + 4u <=
+                     (uint32_t)p.vframe_bytes + 32u);
           uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
           c3[0] = __byte_perm(w0[0], w0[1], pl.y & 0xffffu);
           c3[1] = __byte_perm(w1[0], w1[1], pl.z & 0xffffu);
@@ -768,6 +787,7 @@ render_step_kernel(const RenderParams p) {
             floor_px(p, ex, ez, r[0], r[1], r[2], d, c);
           }
           if (p.mode == PXR_MODE_VIDEO && isinf(d)) {  // distractor.py:172-176
+            PXR_DCHECK(s_rowmap[y] + s_colmap[x] + 3u <= (uint32_t)p.vframe_bytes);
             const uint8_t *t = vsrc + s_rowmap[y] + s_colmap[x];
             c = (uint32_t)t[0] | ((uint32_t)t[1] << 8) | ((uint32_t)t[2] << 16);
           }
@@ -795,6 +815,7 @@ render_step_kernel(const RenderParams p) {
         for (int t = t0; t < t1; t++) {
           const int r = s_rows[t];
           if (r != 0) {
+            PXR_DCHECK(li < p.nt);
             s_ids[li] = (uint16_t)t;
             s_lrp[li] = racc;
             li++;
@@ -843,6 +864,8 @@ render_step_kernel(const RenderParams p) {
         const uint32_t rbase = s_lrp[r0];
         const int n_rows = (int)(s_lrp[r1] - rbase);
         const int n_round = r1 - r0;
+        PXR_DCHECK(r0 < r1 && r1 <= n_live && n_round <= p.cap);
+        PXR_DCHECK(n_rows >= n_round && n_rows <= p.row_cap);
         // records (render.py:366-436), span line equations, row-chunk owners
         for (int li = r0 + tid; li < r1; li += kThreads) {
           const int t = s_ids[li];
@@ -896,6 +919,9 @@ render_step_kernel(const RenderParams p) {
           R.rcp = __drcp_rn((double)area2);
           R.v0 = (uint16_t)i0; R.v1 = (uint16_t)i1; R.v2 = (uint16_t)i2;
           R.flags = (uint16_t)fl;
+          PXR_DCHECK(li - r0 < p.cap && i0 < p.nv && i1 < p.nv && i2 < p.nv);
+          PXR_DCHECK(by0 <= by1 && bx0 <= bx1 && by1 < p.H && bx1 < p.W);
+          PXR_DCHECK(s_lrp[li + 1] - s_lrp[li] == (uint32_t)(by1 - by0 + 1));
           s_rec[li - r0] = R;
           SpanRec S;
           span_setup(a, b, c, (float)(p.H + 1), S);
@@ -907,6 +933,7 @@ render_step_kernel(const RenderParams p) {
           S.row0 = u0;
           s_span[li - r0] = S;
           const uint32_t u1 = u0 + (uint32_t)(by1 - by0 + 1);
+          PXR_DCHECK(((u1 - 1) >> 5) < (uint32_t)(p.row_cap / 32 + 2));
           for (uint32_t k = (u0 + 31) >> 5; k <= ((u1 - 1) >> 5); k++)
             s_rowner[k] = (uint16_t)(li - r0);
         }
@@ -944,17 +971,22 @@ render_step_kernel(const RenderParams p) {
             }
             const uint32_t starts = __reduce_or_sync(kFull, bit);
             const int j = o0 + __popc(starts & lanemask_le);
+            PXR_DCHECK(u >= n_rows || (j < n_round && s_span[j].row0 <= (uint32_t)u &&
+                                       (j + 1 >= n_round || s_span[j + 1].row0 > (uint32_t)u)));
             int len = 0, x0 = 0, row = 0;
             if (u < n_rows) {
               const SpanRec &S = s_span[j];
               row = (int)S.py0 + (u - (int)S.row0);
               len = row_span(S, row, x0);
+              PXR_DCHECK(row >= y0 && row < y1);
+              PXR_DCHECK(len == 0 || (x0 >= 0 && x0 + len <= p.W && len < 0x10000));
             }
             const uint32_t sm = __ballot_sync(kFull, len > 0);
             if (len > 0)
               q[qn + __popc(sm & lanemask_lt)] =
                   make_uint2((uint32_t)x0 | ((uint32_t)len << 16), (uint32_t)row | ((uint32_t)j << 16));
             qn += __popc(sm);
+            PXR_DCHECK(qn <= kQueue);
           }
           while (qn >= 32 || (!more && qn > 0)) {
             __syncwarp();
@@ -993,6 +1025,7 @@ render_step_kernel(const RenderParams p) {
               if (c < N) {
                 const int px = o_x0 + (c - o_ex);
                 pix = (uint32_t)((o_row - y0) * p.W + px);
+                PXR_DCHECK(pix < (uint32_t)npx && o_tri < n_round && owner < 32);
                 cov = eval_exact(s_rec[o_tri], px, o_row, s_vxy64, s_viz, z);
               }
               if (cov) {
@@ -1017,6 +1050,7 @@ render_step_kernel(const RenderParams p) {
           for (int i = tid; i < n_frag; i += kThreads) {
             const uint2 f = s_frag[i];
             const uint32_t pix = f.y & 0xFFFFFu, tri = f.y >> 20;
+            PXR_DCHECK(pix < (uint32_t)npx && tri < (uint32_t)n_round);
             if ((f.x & 0x7FFFFFFFu) == s_dbits[pix]) {  // in S: z < F == z < RN32(z)
               const uint32_t hb = s_wkey[pix] & kDecBit;  // stable after the barrier
               atomicMax(&s_wkey[pix], hb | ((f.x >> 31) ? 0x10000u + tri : 0xFFFFu - tri));
@@ -1036,6 +1070,7 @@ render_step_kernel(const RenderParams p) {
           for (int pass = 0; pass < 2; pass++) {
             for (int u = tid; u < n_rows; u += kThreads) {
               int j = s_rowner[u >> 5];
+              PXR_DCHECK(j < n_round);
               while (j + 1 < n_round && s_span[j + 1].row0 <= (uint32_t)u) j++;
               const SpanRec &S = s_span[j];
               const TriRec &R = s_rec[j];
@@ -1046,6 +1081,7 @@ render_step_kernel(const RenderParams p) {
                 double z;
                 if (!eval_exact(R, px, row, s_vxy64, s_viz, z)) continue;
                 const uint32_t pix = (uint32_t)((row - y0) * p.W + px);
+                PXR_DCHECK(pix < (uint32_t)npx);
                 const uint32_t F = s_dbits[pix];
                 if (__float_as_uint((float)z) != F) continue;
                 if (pass == 0) {
@@ -1241,6 +1277,7 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     p.starts = pack->starts;
     p.counts = pack->counts;
     p.n_videos = pack->n_videos;
+    p.n_frames = pack->n_frames;
     p.Hv = (int)pack->height;
     p.Wv = (int)pack->width;
     p.vframe_bytes = p.Hv * p.Wv * 3;

@@ -18,6 +18,20 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
 
 
+def pytest_sessionstart(session):
+    # tests/test_gpu_checked.py re-runs the GPU suites with PXR_LIB_PATH on
+    # the checked build: make sure that is the library that really loads
+    if os.environ.get("PXR_EXPECT_CHECKED"):
+        from paper_2502_00021_b200 import _native
+
+        assert _native.lib().pxr_build_checked() == 1, _native.LIB_PATH
+
+
+def pytest_terminal_summary(terminalreporter):
+    if os.environ.get("PXR_EXPECT_CHECKED"):
+        terminalreporter.write_line("checked build loaded (PXR_DCHECK on)")
+
+
 def pytest_collection_modifyitems(config, items):
     try:
         import torch

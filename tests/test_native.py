@@ -45,6 +45,21 @@ def test_abi_and_status_strings(native):
     lib = native.lib()
     assert lib.pxr_abi_version() == 1
     assert lib.pxr_status_string(1) == b"invalid argument"
+    if native.LIB_PATH.endswith("libpxr.so"):
+        assert lib.pxr_build_checked() == 0  # the product build has no device checks
+
+
+def test_checked_build_exports_the_same_abi(native):
+    """libpxr_checked.so (make checked): the same kernels with PXR_DCHECK
+    bounds checks, loaded only by tests/test_gpu_checked.py."""
+    path = os.path.join(os.path.dirname(native.LIB_PATH), "libpxr_checked.so")
+    if not os.path.exists(path):
+        subprocess.run(["make", "-s", "-C", native.CSRC, "checked"], check=True)
+    chk = ctypes.CDLL(path)
+    for s in declared_symbols():
+        assert hasattr(chk, s), s
+    chk.pxr_build_checked.restype = ctypes.c_int32
+    assert chk.pxr_build_checked() == 1
 
 
 def test_sm100a_cubin_present(native):
