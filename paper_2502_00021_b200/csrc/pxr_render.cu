@@ -143,6 +143,7 @@ struct RenderParams {
   uint32_t wmagic;  // ceil(2^32 / W): flat pixel index -> row
   int depth_vec;    // out_depth groups of 4 pixels are 16-byte aligned
   int band_h;       // rows per band: a frame is rendered in bands that fit shared memory
+  int scan_sh;      // > 0: live count << scan_sh | bbox rows fits 32 bits (one packed scan)
 };
 
 struct SmemLayout {
@@ -798,20 +799,39 @@ render_step_kernel(const RenderParams p) {
       }
       // block scan over triangles in index order: live ids, bbox-row prefix
       {
-        const int wl = warp_incl_scan(my_live, lane);
-        const int wr = warp_incl_scan(my_rows, lane);
-        if (lane == 31) {
-          s_scan[warp] = wl;
-          s_scan[kWarps + warp] = wr;
+        int li;
+        uint32_t racc;
+        if (p.scan_sh > 0) {
+          // both totals in one word (host bound: nt << scan_sh | nt * band_h
+          // fits 32 bits): one scan instead of two
+          const int sh = p.scan_sh;
+          const uint32_t mine = ((uint32_t)my_live << sh) | (uint32_t)my_rows;
+          const uint32_t w = (uint32_t)warp_incl_scan((int)mine, lane);
+          if (lane == 31) s_scan[warp] = (int)w;
+          __syncthreads();  // (also publishes s_rows and the background)
+          // every warp scans the warp totals itself (no second barrier)
+          const uint32_t v = lane < kWarps ? (uint32_t)s_scan[lane] : 0u;
+          const uint32_t vi = (uint32_t)warp_incl_scan((int)v, lane);
+          if (warp == 0 && lane == kWarps - 1) es.n_live = (int)(vi >> sh);
+          const uint32_t pre = __shfl_sync(kFull, vi - v, warp) + w - mine;
+          li = (int)(pre >> sh);
+          racc = pre & ((1u << sh) - 1u);
+        } else {
+          const int wl = warp_incl_scan(my_live, lane);
+          const int wr = warp_incl_scan(my_rows, lane);
+          if (lane == 31) {
+            s_scan[warp] = wl;
+            s_scan[kWarps + warp] = wr;
+          }
+          __syncthreads();  // (also publishes s_rows and the background)
+          // every warp scans the warp totals itself (no second barrier)
+          const int v = lane < kWarps ? s_scan[lane] : 0;
+          const int u = lane < kWarps ? s_scan[kWarps + lane] : 0;
+          const int vi = warp_incl_scan(v, lane), ui = warp_incl_scan(u, lane);
+          if (warp == 0 && lane == kWarps - 1) es.n_live = vi;
+          li = __shfl_sync(kFull, vi - v, warp) + wl - my_live;
+          racc = (uint32_t)(__shfl_sync(kFull, ui - u, warp) + wr - my_rows);
         }
-        __syncthreads();  // (also publishes s_rows and the background)
-        // every warp scans the warp totals itself (no second barrier)
-        const int v = lane < kWarps ? s_scan[lane] : 0;
-        const int u = lane < kWarps ? s_scan[kWarps + lane] : 0;
-        const int vi = warp_incl_scan(v, lane), ui = warp_incl_scan(u, lane);
-        if (warp == 0 && lane == kWarps - 1) es.n_live = vi;
-        int li = __shfl_sync(kFull, vi - v, warp) + wl - my_live;
-        uint32_t racc = (uint32_t)(__shfl_sync(kFull, ui - u, warp) + wr - my_rows);
         for (int t = t0; t < t1; t++) {
           const int r = s_rows[t];
           if (r != 0) {
@@ -1356,6 +1376,12 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     p.cap = cap;
     if (smem_layout(p).total <= budget || cap <= 16) break;
     cap = cap > 64 ? cap - 32 : cap - 8;
+  }
+  {  // packed block scan: bits for nt * band_h bbox rows + bits for nt live
+    int rb = 0, lb = 0;
+    while (rb < 32 && ((int64_t)1 << rb) <= (int64_t)p.nt * p.band_h) rb++;
+    while (lb < 32 && ((int64_t)1 << lb) <= (int64_t)p.nt) lb++;
+    p.scan_sh = (rb + lb <= 32 && rb < 32 && !getenv("PXR_DEBUG_NO_PACKED_SCAN")) ? rb : 0;
   }
   const int smem = smem_layout(p).total;
   if (smem > budget) return set_unsupported("frame too large for one CTA's shared memory");

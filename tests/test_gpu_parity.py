@@ -111,6 +111,7 @@ class TestRenderGolden:
         {"PXR_DEBUG_CAP": "24", "PXR_DEBUG_FRAG_LIMIT": "0"},
         {"PXR_DEBUG_BAND_H": "20"},                    # row bands (TMA store per band)
         {"PXR_DEBUG_BAND_H": "7", "PXR_DEBUG_CAP": "40"},  # bands + rounds, plain stores
+        {"PXR_DEBUG_NO_PACKED_SCAN": "1", "PXR_DEBUG_CAP": "40"},  # two-scan block scan
     ])
     def test_round_and_overflow_paths_exact(self, torch, pkg, monkeypatch, knobs):
         """The multi-round and fragment-overflow paths (only reached by large
