@@ -88,11 +88,11 @@ static_assert(sizeof(TriRec) == 48, "TriRec layout");
 
 // ... and its conservative row-span data (see span_setup / row_span).
 struct __align__(16) SpanRec {
-  float r[3], c0[3], m[3];  // per edge: x-bound fma(r, y, c0) -/+ margin m,
-                            // or (horizontal edge) c0 = s.y
-  uint16_t px0, px1, py0;
-  uint16_t kinds;           // 2 bits per edge: 0 upper, 1 lower, 2 horiz A>0, 3 horiz A<0
-  uint32_t row0;            // first row unit of the triangle in the round
+  float ur[2], uc[2];  // upper x bounds fma(ur, y, uc) (margin folded into uc)
+  float lr[2], lc[2];  // lower x bounds fma(lr, y, lc)
+  float ylo, yhi;      // rows with ylo <= y <= yhi (horizontal edges; culled: empty)
+  uint16_t py0, pad;
+  uint32_t row0;       // first row unit of the triangle in the round
 };
 static_assert(sizeof(SpanRec) == 48, "SpanRec layout");
 // Non-empty spans wait in a per-warp queue as uint2 {x0 | len << 16,
@@ -379,44 +379,57 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 __device__ __forceinline__ void span_setup(const float2 a, const float2 b, const float2 c,
                                            float ymax, SpanRec &S) {
   const float2 v[3] = {a, b, c};
-  uint32_t kinds = 0;
+  float ur0 = 0.0f, uc0 = 0.0f, ur1 = 0.0f, uc1 = 0.0f;
+  float lr0 = 0.0f, lc0 = 0.0f, lr1 = 0.0f, lc1 = 0.0f;
+  bool have_u = false, have_l = false;
+  float ylo = -__int_as_float(0x7f800000), yhi = __int_as_float(0x7f800000);
 #pragma unroll
   for (int k = 0; k < 3; k++) {
     const float2 s = v[k], t = v[(k + 1) % 3];
     const float A = t.x - s.x, B = t.y - s.y;
-    // horizontal edge (B == 0): only the sign of A * (y - s.y) matters; else
-    // an x bound whose slope only feeds a conservative bound: __fdividef's
-    // <= 2 ulp error moves the line by <= 2^-22 |r| (H + |s.y|), far inside m
-    const bool hz = B == 0.0f;
-    const float r = hz ? 0.0f : __fdividef(A, B);
-    S.r[k] = r;
-    S.c0[k] = hz ? s.y : __fmaf_rn(-r, s.y, s.x);
-    S.m[k] = hz ? 0.0f : 0x1p-10f + (fabsf(s.x) + fabsf(r) * (fabsf(s.y) + ymax)) * 0x1p-17f;
-    kinds |= (hz ? (A > 0.0f ? 2u : 3u) : (B > 0.0f ? 0u : 1u)) << (2 * k);
+    if (B == 0.0f) {
+      // horizontal edge: only the sign of A * (y - s.y) matters, and the f32
+      // comparison of y with s.y is exact
+      if (A > 0.0f) ylo = s.y; else yhi = s.y;
+    } else {
+      // an x bound whose slope only feeds a conservative bound: __fdividef's
+      // <= 2 ulp error moves the line by <= 2^-22 |r| (H + |s.y|), far
+      // inside m; folding m into the intercept adds one rounding of
+      // |c0 + m|, also far inside m
+      const float r = __fdividef(A, B);
+      const float c0 = __fmaf_rn(-r, s.y, s.x);
+      const float m = 0x1p-10f + (fabsf(s.x) + fabsf(r) * (fabsf(s.y) + ymax)) * 0x1p-17f;
+      if (B > 0.0f) {  // bounds x from above
+        ur1 = r; uc1 = c0 + m;
+        if (!have_u) { ur0 = r; uc0 = c0 + m; }
+        have_u = true;
+      } else {
+        lr1 = r; lc1 = c0 - m;
+        if (!have_l) { lr0 = r; lc0 = c0 - m; }
+        have_l = true;
+      }
+    }
   }
-  S.kinds = (uint16_t)kinds;
+  // (a non-degenerate triangle has at least one edge of each kind; a single
+  // one is used twice)
+  S.ur[0] = ur0; S.uc[0] = uc0; S.ur[1] = ur1; S.uc[1] = uc1;
+  S.lr[0] = lr0; S.lc[0] = lc0; S.lr[1] = lr1; S.lc[1] = lc1;
+  S.ylo = ylo;
+  S.yhi = yhi;
 }
 
-// Conservative span of one bbox row: first pixel x0 and length (0 = empty).
-__device__ __forceinline__ int row_span(const SpanRec &S, int py, int &x0) {
+// Conservative span of one bbox row, clamped to the frame: first pixel x0 and
+// length (0 = empty). NaN bounds (overflowing slopes) are ignored by
+// fminf/fmaxf, which only widens the span; the exact test decides each pixel.
+__device__ __forceinline__ int row_span(const SpanRec &S, int py, float wlim, int &x0) {
   const float y = (float)py + 0.5f;
-  float lo = (float)S.px0 + 0.5f, hi = (float)S.px1 + 0.5f;
-  bool empty = false;
-  const uint32_t kinds = S.kinds;
-#pragma unroll
-  for (int k = 0; k < 3; k++) {
-    const uint32_t kind = (kinds >> (2 * k)) & 3u;
-    const float x = __fmaf_rn(S.r[k], y, S.c0[k]);
-    const float ub = __fadd_rn(x, S.m[k]), lb = __fsub_rn(x, S.m[k]);
-    if (kind == 0u) hi = fminf(hi, ub);  // NaN bounds are ignored by fmin/fmax
-    if (kind == 1u) lo = fmaxf(lo, lb);
-    const float dy = y - S.c0[k];  // exact sign of pcy - s.y
-    empty |= (kind == 2u && dy < 0.0f) || (kind == 3u && dy > 0.0f);
-  }
-  const float xa = fmaxf(ceilf(lo - 0.5f), (float)S.px0);
-  const float xb = fminf(floorf(hi - 0.5f), (float)S.px1);
+  const float hi = fminf(fminf(__fmaf_rn(S.ur[0], y, S.uc[0]), __fmaf_rn(S.ur[1], y, S.uc[1])),
+                         wlim);
+  const float lo = fmaxf(fmaxf(__fmaf_rn(S.lr[0], y, S.lc[0]), __fmaf_rn(S.lr[1], y, S.lc[1])),
+                         0.5f);
+  const float xa = ceilf(lo - 0.5f), xb = floorf(hi - 0.5f);
   x0 = (int)xa;
-  return (empty || xa > xb) ? 0 : (int)xb - (int)xa + 1;
+  return (y < S.ylo || y > S.yhi || xa > xb) ? 0 : (int)xb - (int)xa + 1;
 }
 
 // One candidate pixel of triangle R: the reference's exact coverage test and
@@ -521,6 +534,7 @@ render_step_kernel(const RenderParams p) {
   const int warp = tid >> 5;
   const int fpx = p.H * p.W;  // pixels per frame
   const int chans = p.gray ? 1 : 3;
+  const float wlim = (float)p.W - 0.5f;  // last pixel centre
   const double aspect = (double)p.W / (double)p.H;  // render.py:303
   const float ey = p.cam[1];
   const float rx = p.cam[3], ry = p.cam[4], rz = p.cam[5];
@@ -946,9 +960,9 @@ render_step_kernel(const RenderParams p) {
           SpanRec S;
           span_setup(a, b, c, (float)(p.H + 1), S);
           const bool culled = (double)nn < 1e-20;  // degenerate normal (render.py:405-409)
-          S.px0 = (uint16_t)(culled ? 1 : bx0);    // culled: every row span is empty
-          S.px1 = (uint16_t)(culled ? 0 : bx1);
+          if (culled) S.ylo = __int_as_float(0x7f800000);  // every row span is empty
           S.py0 = (uint16_t)by0;
+          S.pad = 0;
           const uint32_t u0 = s_lrp[li] - rbase;
           S.row0 = u0;
           s_span[li - r0] = S;
@@ -997,7 +1011,7 @@ render_step_kernel(const RenderParams p) {
             if (u < n_rows) {
               const SpanRec &S = s_span[j];
               row = (int)S.py0 + (u - (int)S.row0);
-              len = row_span(S, row, x0);
+              len = row_span(S, row, wlim, x0);
               PXR_DCHECK(row >= y0 && row < y1);
               PXR_DCHECK(len == 0 || (x0 >= 0 && x0 + len <= p.W && len < 0x10000));
             }
@@ -1096,7 +1110,7 @@ render_step_kernel(const RenderParams p) {
               const TriRec &R = s_rec[j];
               const int row = (int)S.py0 + (u - (int)S.row0);
               int x0;
-              const int len = row_span(S, row, x0);
+              const int len = row_span(S, row, wlim, x0);
               for (int px = x0; px < x0 + len; px++) {
                 double z;
                 if (!eval_exact(R, px, row, s_vxy64, s_viz, z)) continue;
