@@ -70,6 +70,14 @@ constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kRowCap = 2560;   // bbox rows (>= spans) per raster round (raised to H)
 constexpr int kFragCap = 1536;  // fragment list capacity (overflow: recompute)
 constexpr uint32_t kDecBit = 0x80000000u;
+// debug workload counters per env: live triangles, bbox-row units, non-empty
+// spans, candidate pixels, covered fragments, raster rounds, overflow rounds
+constexpr int kStats = 7;
+#ifdef PXR_CHECKED
+constexpr bool kWithStats = true;  // counters only in the checked build
+#else
+constexpr bool kWithStats = false;
+#endif
 
 constexpr uint32_t kSkyRGB = 135u | (206u << 8) | (235u << 16);  // render.py:50
 
@@ -143,6 +151,7 @@ struct RenderParams {
   uint32_t wmagic;  // ceil(2^32 / W): flat pixel index -> row
   int depth_vec;    // out_depth groups of 4 pixels are 16-byte aligned
   int band_h;       // rows per band: a frame is rendered in bands that fit shared memory
+  int32_t *stats;   // debug (tools/render_stats.py): per env kStats workload counters, or null
   int scan_sh;      // > 0: live count << scan_sh | bbox rows fits 32 bits (one packed scan)
 };
 
@@ -199,6 +208,7 @@ struct EnvShared {
   int n_frag;
   int one_round;  // all live triangles of the band fit one raster round
   int plan_ok;
+  int st[kStats];  // debug counters (p.stats)
 };
 
 // Per-env distractor step (writes the new state back to HBM):
@@ -616,6 +626,7 @@ render_step_kernel(const RenderParams p) {
     // state were prepared by warp kWarps-1 during the previous env) -------
     const int cb = local_env & 1;
     const float4 *s_link_cur = s_link + cb * p.nl;
+    if (kWithStats && p.stats != nullptr && tid < kStats) es.st[tid] = 0;
     if (tid == 0 && p.mode == PXR_MODE_VIDEO && p.vframe_bulk) {
       PXR_DCHECK(es.frame_idx[cb] >= 0 && es.frame_idx[cb] < p.n_frames);
       mbar_arrive_expect_tx(&es.vbar, (uint32_t)p.vframe_bytes);
@@ -898,6 +909,11 @@ render_step_kernel(const RenderParams p) {
         const uint32_t rbase = s_lrp[r0];
         const int n_rows = (int)(s_lrp[r1] - rbase);
         const int n_round = r1 - r0;
+        if (kWithStats && p.stats != nullptr && tid == 0) {
+          es.st[0] += n_round;
+          es.st[1] += n_rows;
+          es.st[5] += 1;
+        }
         PXR_DCHECK(r0 < r1 && r1 <= n_live && n_round <= p.cap);
         PXR_DCHECK(n_rows >= n_round && n_rows <= p.row_cap);
         // records (render.py:366-436), span line equations, row-chunk owners
@@ -1000,7 +1016,8 @@ render_step_kernel(const RenderParams p) {
             const int mi = o0 + 1 + lane;
             uint32_t bit = 0;
             if (mi < n_round) {
-              const int d = (int)s_span[mi].row0 - k * 32;  // >= 1
+              // (row0 of record mi, from the compact prefix: no bank conflicts)
+              const int d = (int)(s_lrp[r0 + mi] - rbase) - k * 32;  // >= 1
               if (d < 32) bit = 1u << d;
             }
             const uint32_t starts = __reduce_or_sync(kFull, bit);
@@ -1020,6 +1037,7 @@ render_step_kernel(const RenderParams p) {
               q[qn + __popc(sm & lanemask_lt)] =
                   make_uint2((uint32_t)x0 | ((uint32_t)len << 16), (uint32_t)row | ((uint32_t)j << 16));
             qn += __popc(sm);
+            if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[2], __popc(sm));
             PXR_DCHECK(qn <= kQueue);
           }
           while (qn >= 32 || (!more && qn > 0)) {
@@ -1039,6 +1057,7 @@ render_step_kernel(const RenderParams p) {
             const int incl = warp_incl_scan(len, lane);
             const int excl = incl - len;
             const int N = __shfl_sync(kFull, incl, 31);
+            if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[3], N);
             for (int c0 = 0; c0 < N; c0 += 32) {
               // span lane of candidate c = c0 + lane: the number of lanes whose
               // inclusive end is <= c (branch-free binary search over the scan)
@@ -1080,6 +1099,10 @@ render_step_kernel(const RenderParams p) {
 
         // exact sequential-order resolve (see the file header)
         const int n_frag = es.n_frag;
+        if (kWithStats && p.stats != nullptr && tid == 0) {
+          es.st[4] += n_frag;
+          es.st[6] += n_frag > p.frag_limit;
+        }
         if (n_frag <= p.frag_limit) {
           for (int i = tid; i < n_frag; i += kThreads) {
             const uint2 f = s_frag[i];
@@ -1151,6 +1174,8 @@ render_step_kernel(const RenderParams p) {
       }
 
       // ---- phase 5: frame -> HBM (one TMA bulk store) --------------------
+      if (kWithStats && p.stats != nullptr && tid < kStats && y0 + band_h >= p.H)
+        p.stats[env * kStats + tid] = es.st[tid];  // (final: last band's resolve ran)
       uint8_t *gout = p.out + (int64_t)env * p.frame_bytes + (int64_t)y0 * p.W * chans;
       const int band_bytes = npx * chans;
       if (p.use_bulk) {  // host: every band's size and offset are multiples of 16
@@ -1352,6 +1377,8 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     if (v > 0) p.row_cap = v > p.H ? v : p.H;
   }
   if (const char *s = getenv("PXR_DEBUG_CAP")) debug_cap = atoi(s);
+  // debug: a device int32 (batch, 7) buffer for per-env workload counters
+  if (const char *s = getenv("PXR_DEBUG_STATS_PTR")) p.stats = (int32_t *)strtoull(s, nullptr, 0);
   int debug_band = 0;
   if (const char *s = getenv("PXR_DEBUG_BAND_H")) debug_band = atoi(s);
 
