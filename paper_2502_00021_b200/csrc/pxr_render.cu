@@ -1057,8 +1057,13 @@ render_step_kernel(const RenderParams p) {
             const int incl = warp_incl_scan(len, lane);
             const int excl = incl - len;
             const int N = __shfl_sync(kFull, incl, 31);
-            if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[3], N);
-            for (int c0 = 0; c0 < N; c0 += 32) {
+            // while spans keep coming only whole rounds of 32 candidates are
+            // evaluated; the rest of the batch goes back on the queue (most
+            // spans hold one pixel, so a batch is ~34 candidates: without
+            // this every batch would end with a nearly empty round)
+            const int NE = more ? (N & ~31) : N;
+            if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[3], NE);
+            for (int c0 = 0; c0 < NE; c0 += 32) {
               // span lane of candidate c = c0 + lane: the number of lanes whose
               // inclusive end is <= c (branch-free binary search over the scan)
               const int c = c0 + lane;
@@ -1075,7 +1080,7 @@ render_step_kernel(const RenderParams p) {
               bool cov = false;
               uint32_t pix = 0;
               double z = 0.0;
-              if (c < N) {
+              if (c < NE) {
                 const int px = o_x0 + (c - o_ex);
                 pix = (uint32_t)((o_row - y0) * p.W + px);
                 PXR_DCHECK(pix < (uint32_t)npx && o_tri < n_round && owner < 32);
@@ -1092,6 +1097,17 @@ render_step_kernel(const RenderParams p) {
                   s_frag[slot] = make_uint2(zb | (z < (double)zf ? 0x80000000u : 0u),
                                             pix | ((uint32_t)o_tri << 20));
               }
+            }
+            if (NE < N) {  // (nb == 32 here, so NE >= 32: progress)
+              const int skip = max(NE - excl, 0);  // pixels of this span already done
+              const bool keep = incl > NE;
+              const uint32_t km = __ballot_sync(kFull, keep);
+              if (keep)
+                q[qn + __popc(km & lanemask_lt)] =
+                    make_uint2((uint32_t)(x0 + skip) | ((uint32_t)(len - skip) << 16),
+                               (uint32_t)row | ((uint32_t)j << 16));
+              qn += __popc(km);
+              PXR_DCHECK(qn <= kQueue);
             }
           }
         }
