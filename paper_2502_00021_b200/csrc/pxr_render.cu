@@ -619,6 +619,10 @@ render_step_kernel(const RenderParams p) {
     prepare_env(p, blockIdx.x, 0, s_link, s_dist, es, lane);
   __syncthreads();
 
+  // liveness: each thread owns a contiguous block of triangles (index order)
+  const int per = (p.nt + kThreads - 1) / kThreads;
+  const int t0 = min(tid * per, p.nt), t1 = min(t0 + per, p.nt);
+
   uint32_t vphase = 0;
   int local_env = 0;
   for (int64_t env = blockIdx.x; env < p.batch; env += gridDim.x, local_env++) {
@@ -635,6 +639,16 @@ render_step_kernel(const RenderParams p) {
     }
     const float ex = es.ex[cb], ez = es.ez[cb];
     bool prepared = env + gridDim.x >= p.batch;  // nothing to prepare for a last env
+
+    // the first liveness triangle's indices, loaded before the vertex phase
+    // so their latency (L2: the geometry does not stay in the small L1 next
+    // to 230 KB of shared memory) overlaps it
+    int n0 = 0, n1 = 0, n2 = 0;  // indices of the next triangle, loaded one ahead
+    if (t0 < t1) {
+      n0 = __ldg(p.tris + 3 * t0 + 0);
+      n1 = __ldg(p.tris + 3 * t0 + 1);
+      n2 = __ldg(p.tris + 3 * t0 + 2);
+    }
 
     // ---- phase 1: world transform + projection (render.py:468-481, 350-363)
     if (p.draw_floor && p.floor_sep) {
@@ -718,13 +732,10 @@ render_step_kernel(const RenderParams p) {
       }
 
       // ---- phase 2: liveness (render.py:366-416) + background -------------
-      // each thread owns a contiguous block of triangles (index order), so
-      // its live count and bbox-row total feed the block scan directly
-      const int per = (p.nt + kThreads - 1) / kThreads;
-      const int t0 = min(tid * per, p.nt), t1 = min(t0 + per, p.nt);
+      // each thread's block of triangles (t0, t1) is contiguous, so its live
+      // count and bbox-row total feed the block scan directly
       int my_live = 0, my_rows = 0;
-      int n0 = 0, n1 = 0, n2 = 0;  // indices of the next triangle, loaded one ahead
-      if (t0 < t1) {
+      if (kBands && y0 > 0 && t0 < t1) {  // (the first band's were loaded at the env's start)
         n0 = __ldg(p.tris + 3 * t0 + 0);
         n1 = __ldg(p.tris + 3 * t0 + 1);
         n2 = __ldg(p.tris + 3 * t0 + 2);
