@@ -1007,7 +1007,10 @@ render_step_kernel(const RenderParams p) {
         // the exact test on them, so the f64 work runs on full warps even
         // though most rows of the thin triangles hold no pixel centre.
         const int n_chunks = (n_rows + 31) >> 5;
-        if (warp == kWarps - 1 && !prepared) {  // joins the chunks afterwards
+        // while warp kWarps-1 prepares the next env the chunks are dealt to
+        // the other warps only (it would otherwise finish last)
+        const int n_workers = prepared ? kWarps : kWarps - 1;
+        if (warp == kWarps - 1 && !prepared) {
           prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
                       lane);
           prepared = true;
@@ -1015,10 +1018,10 @@ render_step_kernel(const RenderParams p) {
         uint2 *q = s_queue + warp * 64;
         int qn = 0;  // queued spans (warp-uniform)
         bool more = true;
-        int k = warp - kWarps;
+        int k = warp - n_workers;
         while (more) {
-          k += kWarps;  // static round-robin over the chunks
-          more = k < n_chunks;
+          k += n_workers;  // static round-robin over the chunks
+          more = k < n_chunks && warp < n_workers;
           if (more) {
             const int u = k * 32 + lane;
             // owner triangle of unit u: the owner of the chunk's first unit plus
