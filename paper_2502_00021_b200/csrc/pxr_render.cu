@@ -496,7 +496,10 @@ __device__ __forceinline__ void put_texel(uint32_t w[3], int k, uint32_t t) {
 }
 
 // kBands = false: the whole frame is one band (y0 = 0, straight-line code).
-template <bool kBands>
+// kFloor = draw_floor: the checker floor needs every thread for the
+// background (f64 per pixel), without it the background is cheap enough for
+// the warps the records phase leaves idle; each kernel compiles one path.
+template <bool kBands, bool kFloor>
 __global__ void __launch_bounds__(kThreads, 1)
 render_step_kernel(const RenderParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -556,7 +559,7 @@ render_step_kernel(const RenderParams p) {
   const uint32_t lanemask_le = 0xFFFFFFFFu >> (31 - lane);
 
   // ---- once per CTA: floor rays, NN maps, mbarrier -----------------------
-  if (p.draw_floor && p.floor_sep) {
+  if (kFloor && p.floor_sep) {
     for (int i = tid; i < p.W; i += kThreads) s_floor[i] = p.floor_rays[(int64_t)i * 3];
     for (int i = tid; i < p.H; i += kThreads) {
       s_floor[p.W + i] = p.floor_rays[(int64_t)i * p.W * 3 + 1];
@@ -651,7 +654,7 @@ render_step_kernel(const RenderParams p) {
     }
 
     // ---- phase 1: world transform + projection (render.py:468-481, 350-363)
-    if (p.draw_floor && p.floor_sep) {
+    if (kFloor && p.floor_sep) {
       // separable floor rays: t = -ez / dz and floor(wy) depend on the row
       // only (render.py:321-334), computed once per row by the last threads
       // (those with no or one vertex below)
@@ -776,63 +779,69 @@ render_step_kernel(const RenderParams p) {
       // or by the resolve's paint, and the distractor composite + grayscale
       // is a per-pixel function of that colour (distractor.py:140-176,
       // env.py:168-173) -- so it is applied at write time (emit) and there is
-      // no separate composite pass. Video: inf pixels take the texel.
-      if (y0 == 0) {  // the env's video frame (one fetch for all bands)
-        if (p.mode == PXR_MODE_VIDEO && p.vframe_bulk) mbar_wait_parity(&es.vbar, vphase);
-        vphase ^= 1u;
-      }
-      if (p.mode == PXR_MODE_VIDEO && !p.draw_floor && plan_ok && !p.gray) {
-        // 4-pixel groups: three texel words through the byte-permute plan
-        const float inf = __int_as_float(0x7f800000);
-        const int n4 = npx >> 2;  // plan_ok: W % 4 == 0, no tail
-        for (int gi = tid; gi < n4; gi += kThreads) {
-          const int i0 = gi << 2;
-          const int yb = (int)__umulhi((uint32_t)i0, p.wmagic);
-          const uint4 pl = s_gplan[(i0 - yb * p.W) >> 2];
-          const uint32_t *src =
-              reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y0 + yb]) + pl.x;
-          const uint32_t *w0 = src + (pl.y >> 16), *w1 = src + (pl.z >> 16),
-                         *w2 = src + (pl.w >> 16);
-          PXR_DCHECK(4u * (uint32_t)(w0 + 1 - reinterpret_cast<const uint32_t *>(s_vframe)) + 4u <=
-                     (uint32_t)p.vframe_bytes + 32u);
-          PXR_DCHECK(4u * (uint32_t)(w2 + 1 - reinterpret_cast<const uint32_t *>(s_vframe)) + 4u <=
-                     (uint32_t)p.vframe_bytes + 32u);
-          uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
-          c3[0] = __byte_perm(w0[0], w0[1], pl.y & 0xffffu);
-          c3[1] = __byte_perm(w1[0], w1[1], pl.z & 0xffffu);
-          c3[2] = __byte_perm(w2[0], w2[1], pl.w & 0xffffu);
-          reinterpret_cast<float4 *>(s_depth)[gi] = make_float4(inf, inf, inf, inf);
-          reinterpret_cast<uint4 *>(s_wkey)[gi] = make_uint4(0u, 0u, 0u, 0u);
-        }
-      } else {
-        for (int i = tid; i < npx; i += kThreads) {
-          const int yb = (int)__umulhi((uint32_t)i, p.wmagic), x = i - yb * p.W;
-          const int y = y0 + yb;
-          float d = __int_as_float(0x7f800000);
-          uint32_t c = kSkyRGB;
-          if (p.draw_floor && p.floor_sep) {
-            const int k = s_fk[y];
-            if (k >= 0) {  // same arithmetic as floor_px with the row terms hoisted
-              const double t = s_ft[y];
-              const double wx = (double)ex + t * s_floor[x];
-              const uint32_t g = ((uint32_t)__double2ll_rd(wx) ^ (uint32_t)k) & 1u ? 122u : 158u;
-              c = g | (g << 8) | (g << 16);
-              d = (float)t;
+      // no separate composite pass. Video: inf pixels take the texel. Without
+      // a floor (cheap texel / sky pixels) it is written by the warps the
+      // records phase leaves idle (see below), else here by every thread:
+      // threads first, first + stride, ...
+      const bool vwait = y0 == 0 && p.mode == PXR_MODE_VIDEO && p.vframe_bulk;
+      const uint32_t vpar = vphase;
+      if (y0 == 0) vphase ^= 1u;  // the env's video frame (one fetch for all bands)
+      auto background = [&](int first, int stride) {
+        if (vwait) mbar_wait_parity(&es.vbar, vpar);
+        if (p.mode == PXR_MODE_VIDEO && !kFloor && plan_ok && !p.gray) {
+          // 4-pixel groups: three texel words through the byte-permute plan
+          const float inf = __int_as_float(0x7f800000);
+          const int n4 = npx >> 2;  // plan_ok: W % 4 == 0, no tail
+          for (int gi = first; gi < n4; gi += stride) {
+            const int i0 = gi << 2;
+            const int yb = (int)__umulhi((uint32_t)i0, p.wmagic);
+            const uint4 pl = s_gplan[(i0 - yb * p.W) >> 2];
+            const uint32_t *src =
+                reinterpret_cast<const uint32_t *>(s_vframe + s_rowmap[y0 + yb]) + pl.x;
+            const uint32_t *w0 = src + (pl.y >> 16), *w1 = src + (pl.z >> 16),
+                           *w2 = src + (pl.w >> 16);
+            PXR_DCHECK(4u * (uint32_t)(w0 + 1 - reinterpret_cast<const uint32_t *>(s_vframe)) + 4u <=
+                       (uint32_t)p.vframe_bytes + 32u);
+            PXR_DCHECK(4u * (uint32_t)(w2 + 1 - reinterpret_cast<const uint32_t *>(s_vframe)) + 4u <=
+                       (uint32_t)p.vframe_bytes + 32u);
+            uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
+            c3[0] = __byte_perm(w0[0], w0[1], pl.y & 0xffffu);
+            c3[1] = __byte_perm(w1[0], w1[1], pl.z & 0xffffu);
+            c3[2] = __byte_perm(w2[0], w2[1], pl.w & 0xffffu);
+            reinterpret_cast<float4 *>(s_depth)[gi] = make_float4(inf, inf, inf, inf);
+            reinterpret_cast<uint4 *>(s_wkey)[gi] = make_uint4(0u, 0u, 0u, 0u);
+          }
+        } else {
+          for (int i = first; i < npx; i += stride) {
+            const int yb = (int)__umulhi((uint32_t)i, p.wmagic), x = i - yb * p.W;
+            const int y = y0 + yb;
+            float d = __int_as_float(0x7f800000);
+            uint32_t c = kSkyRGB;
+            if (kFloor && p.floor_sep) {
+              const int k = s_fk[y];
+              if (k >= 0) {  // same arithmetic as floor_px with the row terms hoisted
+                const double t = s_ft[y];
+                const double wx = (double)ex + t * s_floor[x];
+                const uint32_t g = ((uint32_t)__double2ll_rd(wx) ^ (uint32_t)k) & 1u ? 122u : 158u;
+                c = g | (g << 8) | (g << 16);
+                d = (float)t;
+              }
+            } else if (kFloor) {
+              const double *r = p.floor_rays + ((int64_t)y0 * p.W + i) * 3;
+              floor_px(p, ex, ez, r[0], r[1], r[2], d, c);
             }
-          } else if (p.draw_floor) {
-            const double *r = p.floor_rays + ((int64_t)y0 * p.W + i) * 3;
-            floor_px(p, ex, ez, r[0], r[1], r[2], d, c);
+            if (p.mode == PXR_MODE_VIDEO && isinf(d)) {  // distractor.py:172-176
+              PXR_DCHECK(s_rowmap[y] + s_colmap[x] + 3u <= (uint32_t)p.vframe_bytes);
+              const uint8_t *t = vsrc + s_rowmap[y] + s_colmap[x];
+              c = (uint32_t)t[0] | ((uint32_t)t[1] << 8) | ((uint32_t)t[2] << 16);
+            }
+            s_depth[i] = d;
+            s_wkey[i] = 0u;
+            emit((uint32_t)i, c);
           }
-          if (p.mode == PXR_MODE_VIDEO && isinf(d)) {  // distractor.py:172-176
-            PXR_DCHECK(s_rowmap[y] + s_colmap[x] + 3u <= (uint32_t)p.vframe_bytes);
-            const uint8_t *t = vsrc + s_rowmap[y] + s_colmap[x];
-            c = (uint32_t)t[0] | ((uint32_t)t[1] << 8) | ((uint32_t)t[2] << 16);
-          }
-          s_depth[i] = d;
-          s_wkey[i] = 0u;
-          emit((uint32_t)i, c);
         }
-      }
+      };
+      if (kFloor) background(tid, kThreads);
       // block scan over triangles in index order: live ids, bbox-row prefix
       {
         int li;
@@ -844,7 +853,7 @@ render_step_kernel(const RenderParams p) {
           const uint32_t mine = ((uint32_t)my_live << sh) | (uint32_t)my_rows;
           const uint32_t w = (uint32_t)warp_incl_scan((int)mine, lane);
           if (lane == 31) s_scan[warp] = (int)w;
-          __syncthreads();  // (also publishes s_rows and the background)
+          __syncthreads();  // (also publishes s_rows and a floor background)
           // every warp scans the warp totals itself (no second barrier)
           const uint32_t v = lane < kWarps ? (uint32_t)s_scan[lane] : 0u;
           const uint32_t vi = (uint32_t)warp_incl_scan((int)v, lane);
@@ -859,7 +868,7 @@ render_step_kernel(const RenderParams p) {
             s_scan[warp] = wl;
             s_scan[kWarps + warp] = wr;
           }
-          __syncthreads();  // (also publishes s_rows and the background)
+          __syncthreads();  // (also publishes s_rows and a floor background)
           // every warp scans the warp totals itself (no second barrier)
           const int v = lane < kWarps ? s_scan[lane] : 0;
           const int u = lane < kWarps ? s_scan[kWarps + lane] : 0;
@@ -893,6 +902,10 @@ render_step_kernel(const RenderParams p) {
       __syncthreads();
       const int n_live = es.n_live;
       const bool one_round = es.one_round != 0;
+      if (!kFloor && n_live == 0) {
+        background(tid, kThreads);
+        __syncthreads();  // (the depth output reads it)
+      }
 
       // ---- phases 3/4: raster rounds over live triangles in index order ---
       for (int r0 = 0; r0 < n_live;) {
@@ -927,7 +940,12 @@ render_step_kernel(const RenderParams p) {
         }
         PXR_DCHECK(r0 < r1 && r1 <= n_live && n_round <= p.cap);
         PXR_DCHECK(n_rows >= n_round && n_rows <= p.row_cap);
-        // records (render.py:366-436), span line equations, row-chunk owners
+        // records (render.py:366-436), span line equations, row-chunk owners;
+        // in the first round the warps without a record write the background
+        // meanwhile (all threads after their records if fewer than 4 are free)
+        const int rec_warps = min((n_round + 31) >> 5, kWarps);
+        const bool bg_here = !kFloor && r0 == 0;
+        const bool bg_split = bg_here && rec_warps <= kWarps - 4;
         for (int li = r0 + tid; li < r1; li += kThreads) {
           const int t = s_ids[li];
           int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
@@ -998,6 +1016,10 @@ render_step_kernel(const RenderParams p) {
           for (uint32_t k = (u0 + 31) >> 5; k <= ((u1 - 1) >> 5); k++)
             s_rowner[k] = (uint16_t)(li - r0);
         }
+        // (warps without records arrive here at once)
+        if (bg_here && (!bg_split || warp >= rec_warps))
+          background(bg_split ? tid - rec_warps * 32 : tid,
+                     bg_split ? kThreads - rec_warps * 32 : kThreads);
         __syncthreads();
 
         // (triangle, bbox row) units, 32 per chunk, chunks dealt round-robin
@@ -1457,7 +1479,10 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   const int smem = smem_layout(p).total;
   if (smem > budget) return set_unsupported("frame too large for one CTA's shared memory");
   const bool banded = p.band_h < p.H;
-  auto kernel = banded ? render_step_kernel<true> : render_step_kernel<false>;
+  auto kernel = banded ? (p.draw_floor ? render_step_kernel<true, true>
+                                       : render_step_kernel<true, false>)
+                       : (p.draw_floor ? render_step_kernel<false, true>
+                                       : render_step_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
   int per_sm = 0;
