@@ -626,6 +626,18 @@ render_step_kernel(const RenderParams p) {
   const int per = (p.nt + kThreads - 1) / kThreads;
   const int t0 = min(tid * per, p.nt), t1 = min(t0 + per, p.nt);
 
+  // the (env-independent) base geometry of this thread's first vertex stays
+  // in registers: no global-load latency at the start of every env
+  int g_link = 0;
+  float g_bx = 0.0f, g_by = 0.0f, g_bz = 0.0f;
+  if (tid < p.nv) {
+    g_link = __ldg(p.vert_link + tid);
+    PXR_DCHECK(g_link >= 0 && g_link < p.nl);
+    g_bx = __ldg(p.base_verts + 3 * tid + 0);
+    g_by = __ldg(p.base_verts + 3 * tid + 1);
+    g_bz = __ldg(p.base_verts + 3 * tid + 2);
+  }
+
   uint32_t vphase = 0;
   int local_env = 0;
   for (int64_t env = blockIdx.x; env < p.batch; env += gridDim.x, local_env++) {
@@ -674,7 +686,13 @@ render_step_kernel(const RenderParams p) {
       }
     }
     for (int v = tid; v < p.nv; v += kThreads) {
-      const float3 w = world_vertex(p, s_link_cur, v);
+      float3 w;
+      if (v == tid) {  // the thread's first vertex: geometry held in registers
+        const float4 lk = s_link_cur[g_link];
+        w = make_float3(lk.x + g_bx * lk.z - g_bz * lk.w, g_by, lk.y + g_bx * lk.w + g_bz * lk.z);
+      } else {
+        w = world_vertex(p, s_link_cur, v);
+      }
       s_world[3 * v + 0] = w.x;
       s_world[3 * v + 1] = w.y;
       s_world[3 * v + 2] = w.z;
