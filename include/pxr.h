@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PXR_ABI_VERSION 1
+#define PXR_ABI_VERSION 2
 
 typedef int32_t pxr_status;
 #define PXR_OK 0
@@ -94,6 +94,10 @@ typedef struct pxr_step_keys {
   uint64_t key_hi, key_lo;   /* key_t = fold_in(master, t)                 */
   uint64_t env_offset;       /* global index of env 0 of this batch        */
   uint64_t logical_batch;    /* reset keys use fold_in(key_t, LB + g)      */
+  /* optional: key_t as (hi, lo) in DEVICE memory, read when the kernel runs
+   * (key_hi/key_lo ignored) -- a captured CUDA graph replays with the key
+   * pxr_step_key_advance wrote for this step */
+  const uint64_t *device_key;
 } pxr_step_keys;
 
 /* ------------------------------------------------------------------ */
@@ -217,7 +221,13 @@ pxr_status pxr_reset_envs(const pxr_model *model, double *qpos, double *qvel,
                           int64_t *ep_length, double *info_return, int64_t *info_length,
                           const double *reward, int64_t batch, uint64_t key_hi,
                           uint64_t key_lo, uint64_t env_offset, uint64_t logical_batch,
-                          int32_t mode, void *stream);
+                          int32_t mode, const uint64_t *device_key, void *stream);
+
+/* key_t = fold_in(master, *t) into key_out[0..1] (device), then *t += 1:
+ * the per-step key schedule of env.py:209 on the device, so a CUDA graph of
+ * the env step stays valid from one replay to the next. */
+pxr_status pxr_step_key_advance(uint64_t master_hi, uint64_t master_lo, int64_t *t,
+                                uint64_t *key_out, void *stream);
 
 /* forward_kinematics for an env's model: qpos (B, L + 2) -> poses (B, L, 3). */
 pxr_status pxr_env_poses(const pxr_model *model, const double *qpos, int64_t batch,

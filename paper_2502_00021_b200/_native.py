@@ -32,6 +32,7 @@ EXPORTED = (
     "pxr_apply_color", "pxr_apply_video", "pxr_grayscale", "pxr_threefry2x64",
     "pxr_sincosf", "pxr_pose_source", "pxr_forward_kinematics", "pxr_div_check",
     "pxr_physics_step", "pxr_reset_envs", "pxr_env_poses", "pxr_conv_stub_forward",
+    "pxr_step_key_advance",
 )
 
 _vp = ctypes.c_void_p
@@ -71,7 +72,7 @@ class VideoPackC(ctypes.Structure):
 
 class StepKeys(ctypes.Structure):
     _fields_ = [("key_hi", _u64), ("key_lo", _u64), ("env_offset", _u64),
-                ("logical_batch", _u64)]
+                ("logical_batch", _u64), ("device_key", _vp)]
 
 
 class Model(ctypes.Structure):
@@ -153,11 +154,13 @@ def lib() -> ctypes.CDLL:
     L.pxr_physics_step.argtypes = [P(Model), _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]
     L.pxr_reset_envs.restype = _i32
     L.pxr_reset_envs.argtypes = [P(Model), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
-                                 _u64, _u64, _u64, _u64, _i32, _vp]
+                                 _u64, _u64, _u64, _u64, _i32, _vp, _vp]
+    L.pxr_step_key_advance.restype = _i32
+    L.pxr_step_key_advance.argtypes = [_u64, _u64, _vp, _vp, _vp]
     L.pxr_env_poses.restype = _i32
     L.pxr_env_poses.argtypes = [P(Model), _vp, _i64, _vp, _vp]
-    if L.pxr_abi_version() != 1:
-        raise ImportError(f"{LIB_PATH}: ABI version {L.pxr_abi_version()} != 1")
+    if L.pxr_abi_version() != 2:
+        raise ImportError(f"{LIB_PATH}: ABI version {L.pxr_abi_version()} != 2")
     _lib = L
     return L
 

@@ -151,10 +151,13 @@ class BenchConfig:
 
 def _bench_one(config: BenchConfig, env_name: str, batch: int, mode: str) -> BenchRecord:
     """bench.py:183-216: policy forward + env step per iteration, everything
-    on the device; the clock stops after the device has finished."""
+    on the device; the clock stops after the device has finished. The
+    iteration is one replay of a CUDA graph of (policy, step) (env.StepGraph:
+    same results as the step loop, bit for bit; at small batches the loop is
+    otherwise launch-bound)."""
     import torch
 
-    from .env import EnvConfig, make_env, step
+    from .env import EnvConfig, StepGraph, make_env
 
     cfg = EnvConfig(model=env_name, batch=batch, width=config.width, height=config.height,
                     distractor_mode=mode,
@@ -163,16 +166,14 @@ def _bench_one(config: BenchConfig, env_name: str, batch: int, mode: str) -> Ben
     env, state, obs = make_env(cfg)
     stub = ConvStub.create(config.height, config.width, int(obs.shape[-1]), env.n_joints,
                            seed=config.seed)
-    for _ in range(config.warmup_steps):
-        state, out = step(env, state, conv_stub_forward(stub, obs))
-        obs = out.obs
+    g = StepGraph(env, state, obs, lambda o: conv_stub_forward(stub, o))
+    g.replay(config.warmup_steps)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(config.measure_steps):
-        state, out = step(env, state, conv_stub_forward(stub, obs))
-        obs = out.obs
+    g.replay(config.measure_steps)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    obs = g.obs
     steps = batch * config.measure_steps
     return BenchRecord(env_name=env_name, batch=batch, distractor_mode=mode,
                        steps_measured=steps, wall_seconds=wall, steps_per_second=steps / wall,

@@ -226,6 +226,16 @@ __global__ void pose_source_kernel(const double *rest, const int32_t *parent,
   }
 }
 
+// key_t = fold_in(master, t) = TF(master, (t, 2)) (prng.py:105-108), t += 1
+__global__ void step_key_kernel(uint64_t mhi, uint64_t mlo, int64_t *t, uint64_t *key_out) {
+  const int64_t tt = *t;
+  uint64_t hi, lo;
+  threefry2x64(mhi, mlo, (uint64_t)tt, 2, hi, lo);
+  key_out[0] = hi;
+  key_out[1] = lo;
+  *t = tt + 1;
+}
+
 }  // namespace pxr
 
 using namespace pxr;
@@ -282,6 +292,8 @@ extern "C" pxr_status pxr_advance_distractors(const pxr_distractor *dist,
                                               const pxr_step_keys *keys, const uint8_t *done,
                                               void *stream) {
   if (dist == nullptr || keys == nullptr) return set_invalid("null state/keys");
+  if (keys->device_key != nullptr)
+    return set_unsupported("pxr_advance_distractors takes host keys (device_key: pxr_render_step)");
   if (batch < 1) return set_invalid("batch must be >= 1");
   if (dist->mode == PXR_MODE_NONE) return PXR_OK;
   if (dist->mode == PXR_MODE_COLOR && dist->color_bias == nullptr)
@@ -352,6 +364,13 @@ extern "C" pxr_status pxr_threefry2x64(const uint64_t *k0, const uint64_t *k1,
   threefry_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
       k0, k1, key_stride ? 1 : 0, c0, c1, c1_stride ? 1 : 0, y0, y1, n);
   return check_launch("threefry_kernel");
+}
+
+extern "C" pxr_status pxr_step_key_advance(uint64_t master_hi, uint64_t master_lo, int64_t *t,
+                                           uint64_t *key_out, void *stream) {
+  if (t == nullptr || key_out == nullptr) return set_invalid("pxr_step_key_advance: null argument");
+  step_key_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(master_hi, master_lo, t, key_out);
+  return check_launch("step_key_kernel");
 }
 
 extern "C" pxr_status pxr_sincosf(const float *x, float *s, float *c, int64_t n, void *stream) {

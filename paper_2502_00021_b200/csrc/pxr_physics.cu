@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/pxr.h"
 #include "pxr_internal.cuh"
@@ -300,6 +301,214 @@ __global__ void physics_step_kernel(StepArgs a) {
   }
 }
 
+// The same control step with one WARP per env (small and medium batches,
+// where one thread per env leaves the GPU idle and the per-env chain is the
+// latency): per substep the link trig, contacts, torques and integration
+// run one link / dof per lane, the mass-matrix columns (one RNEA pass each)
+// and the bias pass run on separate lanes, and the Cholesky factor is built
+// column by column with its rows in parallel. Every element is computed by
+// the same operations in the same order as physics_step_kernel, so the two
+// kernels agree bit for bit (tests/test_physics_api.py).
+constexpr int kPhysWarps = 4;  // envs per block
+
+struct WarpPhys {
+  double qb[kMaxD], qdb[kMaxD], q0[kMaxD], tau[kMaxD], bias[kMaxD], rhs[kMaxD], qdd[kMaxD];
+  double M[kMaxD * kMaxD];
+  double theta[kMaxL], ct[kMaxL], st[kMaxL], omega[kMaxL], ox[kMaxL], oz[kMaxL], vox[kMaxL],
+      voz[kMaxL], fex[kMaxL], fez[kMaxL], tex[kMaxL];
+};
+
+__global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(StepArgs a) {
+  __shared__ WarpPhys s_env[kPhysWarps];
+  const Model &m = a.m;
+  const int nl = m.nl, nd = nl + 2, nj = nd - 3;
+  const int active0 = a.fixed_root ? 3 : 0;
+  const int lane = threadIdx.x & 31;
+  WarpPhys &S = s_env[threadIdx.x >> 5];
+  PXR_DCHECK(nl >= 1 && nl <= kMaxL && nd <= kMaxD && nd < 32 && m.parent[0] < 0);
+  for (int64_t b = (int64_t)blockIdx.x * kPhysWarps + (threadIdx.x >> 5); b < a.batch;
+       b += (int64_t)gridDim.x * kPhysWarps) {
+    double *q = a.qpos + b * nd, *qd = a.qvel + b * nd;
+    const double *act = a.actions + b * nj;
+    if (lane < nd) {
+      S.qb[lane] = q[lane];
+      S.qdb[lane] = qd[lane];
+      S.q0[lane] = q[lane];
+    }
+    __syncwarp();
+    const double x_before = S.qb[0];
+    for (int sub = 0; sub < a.substeps; sub++) {
+      // kinematics pass (physics.py:144-163): angle chain, per-link trig,
+      // velocity chain
+      if (lane == 0) {
+        S.theta[0] = S.qb[2];
+        for (int i = 1; i < nl; i++) S.theta[i] = S.theta[m.parent[i]] + S.qb[3 + i - 1];
+      }
+      __syncwarp();
+      if (lane < nl) {
+        S.ct[lane] = cos(S.theta[lane]);
+        S.st[lane] = sin(S.theta[lane]);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        S.omega[0] = S.qdb[2];
+        S.ox[0] = S.qb[0]; S.oz[0] = S.qb[1];
+        S.vox[0] = S.qdb[0]; S.voz[0] = S.qdb[1];
+        for (int i = 1; i < nl; i++) {
+          const int p = m.parent[i];
+          const double c = S.ct[p], s = S.st[p];
+          const double ad = m.adist[i];
+          S.ox[i] = S.ox[p] + ad * c;
+          S.oz[i] = S.oz[p] + ad * s;
+          S.vox[i] = S.vox[p] + S.omega[p] * ad * (-s);
+          S.voz[i] = S.voz[p] + S.omega[p] * ad * c;
+          S.omega[i] = S.omega[p] + S.qdb[3 + i - 1];
+        }
+      }
+      __syncwarp();
+      // ground contact at both capsule ends (physics.py:321-353), one link per lane
+      if (lane < nl) {
+        const int i = lane;
+        const double c = S.ct[i], s = S.st[i];
+        double fx = 0.0, fz = 0.0, tx = 0.0;
+        for (int end = 0; end < 2; end++) {
+          double px, pz, vx, vz;
+          if (end == 0) {
+            px = S.ox[i]; pz = S.oz[i]; vx = S.vox[i]; vz = S.voz[i];
+          } else {
+            px = S.ox[i] + m.length[i] * c;
+            pz = S.oz[i] + m.length[i] * s;
+            vx = S.vox[i] + S.omega[i] * m.length[i] * (-s);
+            vz = S.voz[i] + S.omega[i] * m.length[i] * c;
+          }
+          if (pz < 0.0) {
+            double fn = -CONTACT_SPRING * pz - CONTACT_DAMPING * vz;
+            if (fn < 0.0) fn = 0.0;
+            double ft = -FRICTION_GAIN * vx;
+            const double cap = FRICTION_MU * fn;
+            if (ft > cap) ft = cap;
+            else if (ft < -cap) ft = -cap;
+            fx += ft;
+            fz += fn;
+            const double rxx = px - S.ox[i], rzz = pz - S.oz[i];
+            tx += rxx * fn - rzz * ft;
+          }
+        }
+        S.fex[i] = fx;
+        S.fez[i] = fz;
+        S.tex[i] = tx;
+      }
+      // actuation + joint-limit penalty (physics.py:355-370), one dof per lane
+      if (lane < nd) {
+        double t = 0.0;
+        if (lane >= 3) {
+          const int j = lane - 3;
+          double av = act[j];
+          if (av > 1.0) av = 1.0;
+          else if (av < -1.0) av = -1.0;
+          t = av * m.torque_max[j];
+          const double qj = S.qb[3 + j];
+          if (qj < m.limit_lo[j]) t += LIMIT_SPRING * (m.limit_lo[j] - qj) - LIMIT_DAMPING * S.qdb[3 + j];
+          else if (qj > m.limit_hi[j]) t -= LIMIT_SPRING * (qj - m.limit_hi[j]) + LIMIT_DAMPING * S.qdb[3 + j];
+          t -= JOINT_DAMPING * S.qdb[3 + j];
+        }
+        S.tau[lane] = t;
+      }
+      __syncwarp();
+      // RNEA bias (lane 31) and the mass-matrix columns (lane j)
+      if (lane == 31 || (lane >= active0 && lane < nd)) {
+        double zeros[kMaxD], vec[kMaxD], col[kMaxD];
+        for (int d = 0; d < nd; d++) {
+          zeros[d] = 0.0;
+          vec[d] = d == lane ? 1.0 : 0.0;
+        }
+        if (lane == 31) {
+          rnea(m, S.qb, S.qdb, zeros, S.ct, S.st, GRAVITY, S.fex, S.fez, S.tex, true, col);
+          for (int d = 0; d < nd; d++) S.bias[d] = col[d];
+        } else {
+          rnea(m, S.qb, zeros, vec, S.ct, S.st, 0.0, S.fex, S.fez, S.tex, false, col);
+          for (int i = 0; i < nd; i++) S.M[i * kMaxD + lane] = col[i];
+        }
+      }
+      __syncwarp();
+      if (lane < nd) S.rhs[lane] = S.tau[lane] - S.bias[lane];
+      // Cholesky (physics.py:241-269 / solve_spd): column j, then its rows
+      for (int j = active0; j < nd; j++) {
+        if (lane == 0) {
+          double acc = S.M[j * kMaxD + j];
+          for (int t = active0; t < j; t++) acc -= S.M[j * kMaxD + t] * S.M[j * kMaxD + t];
+          if (acc < 1e-12) acc = 1e-12;
+          S.M[j * kMaxD + j] = sqrt(acc);
+        }
+        __syncwarp();
+        const int i = lane;
+        if (i > j && i < nd) {
+          double acc = S.M[i * kMaxD + j];
+          for (int t = active0; t < j; t++) acc -= S.M[i * kMaxD + t] * S.M[j * kMaxD + t];
+          S.M[i * kMaxD + j] = acc / S.M[j * kMaxD + j];
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {  // the two triangular solves
+        double *x = S.qdd;
+        for (int i = 0; i < active0; i++) x[i] = 0.0;
+        for (int i = active0; i < nd; i++) {
+          double acc = S.rhs[i];
+          for (int t = active0; t < i; t++) acc -= S.M[i * kMaxD + t] * x[t];
+          x[i] = acc / S.M[i * kMaxD + i];
+        }
+        for (int i = nd - 1; i >= active0; i--) {
+          double acc = x[i];
+          for (int t = i + 1; t < nd; t++) acc -= S.M[t * kMaxD + i] * x[t];
+          x[i] = acc / S.M[i * kMaxD + i];
+        }
+      }
+      __syncwarp();
+      if (lane < nd) {  // semi-implicit Euler (physics.py:389-398)
+        const int d = lane;
+        double v = S.qdb[d] + a.h * S.qdd[d];
+        if (v > VEL_CLAMP) v = VEL_CLAMP;
+        else if (v < -VEL_CLAMP) v = -VEL_CLAMP;
+        S.qdb[d] = v;
+        S.qb[d] += a.h * v;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      // non-finite guard (physics.py:401-412)
+      bool finite = true;
+      for (int d = 0; d < nd; d++) {
+        if (!(isfinite(S.qb[d]) && isfinite(S.qdb[d]))) finite = false;
+        else if (S.qb[d] > DIVERGED || S.qb[d] < -DIVERGED) finite = false;
+      }
+      if (!finite) {
+        for (int d = 0; d < nd; d++) {
+          S.qb[d] = S.q0[d];
+          S.qdb[d] = 0.0;
+        }
+        a.done[b] = 1;
+      }
+      for (int d = 0; d < nd; d++) {
+        q[d] = S.qb[d];
+        qd[d] = S.qdb[d];
+      }
+      a.step_count[b] += 1;
+      if (a.step_count[b] >= a.ep_len) a.done[b] = 1;
+      if (a.has_min_h && q[1] < a.min_h) a.done[b] = 1;
+      // compute_reward (physics.py:468-477) on this control step
+      double sq[kMaxD];
+      for (int j = 0; j < nj; j++) {
+        double av = act[j];
+        av = av > 1.0 ? 1.0 : (av < -1.0 ? -1.0 : av);
+        sq[j] = av * av;
+      }
+      const double forward = (q[0] - x_before) / a.dt;
+      a.reward[b] += a.forward_weight * forward - a.ctrl_cost * np_sum(sq, nj);
+    }
+    __syncwarp();
+  }
+}
+
 // prng.py:124-135 uniform(key, n, lo, hi) draws for one key into out[0..n)
 __device__ void uniform_draws(uint64_t khi, uint64_t klo, int n, double lo, double hi,
                               double *out) {
@@ -346,7 +555,12 @@ __global__ void reset_kernel(const double *rest, int nd, double *qpos, double *q
                              int64_t *step_count, uint8_t *done, double *ep_return,
                              int64_t *ep_length, double *info_return, int64_t *info_length,
                              const double *reward, int64_t batch, uint64_t khi, uint64_t klo,
-                             uint64_t env_offset, uint64_t logical_batch, int mode) {
+                             uint64_t env_offset, uint64_t logical_batch, int mode,
+                             const uint64_t *dkey) {
+  if (dkey != nullptr) {  // key_t written on the device this step (graph replay)
+    khi = dkey[0];
+    klo = dkey[1];
+  }
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch;
        b += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t g = env_offset + (uint64_t)b;
@@ -407,6 +621,10 @@ __global__ void fk_env_kernel(const double *qpos, const int32_t *parent, const d
   }
 }
 
+// measured crossover (tools/phys_bench.py, B200): warp-per-env is 1.6-2.4x
+// faster up to ~1-2k envs, one thread per env wins from ~4k on
+constexpr int64_t kWarpEnvMax = 2048;
+
 static inline unsigned blocks_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -447,6 +665,16 @@ extern "C" pxr_status pxr_physics_step(const pxr_model *model, double *qpos, dou
   a.forward_weight = model->forward_weight;
   a.ctrl_cost = model->ctrl_cost;
   a.ep_len = model->episode_length;
+  // one warp per env up to kWarpEnvMax envs (latency-bound range), one
+  // thread per env above (throughput); PXR_DEBUG_PHYS=warp|thread forces one
+  const char *force = getenv("PXR_DEBUG_PHYS");
+  bool warp = batch <= kWarpEnvMax;
+  if (force != nullptr) warp = force[0] == 'w';
+  if (warp) {
+    physics_step_warp_kernel<<<blocks_for((batch + kPhysWarps - 1) / kPhysWarps, 1),
+                               kPhysWarps * 32, 0, (cudaStream_t)stream>>>(a);
+    return check_launch("physics_step_warp_kernel");
+  }
   physics_step_kernel<<<blocks_for(batch, 64), 64, 0, (cudaStream_t)stream>>>(a);
   return check_launch("physics_step_kernel");
 }
@@ -456,7 +684,8 @@ extern "C" pxr_status pxr_reset_envs(const pxr_model *model, double *qpos, doubl
                                      int64_t *ep_length, double *info_return,
                                      int64_t *info_length, const double *reward, int64_t batch,
                                      uint64_t key_hi, uint64_t key_lo, uint64_t env_offset,
-                                     uint64_t logical_batch, int32_t mode, void *stream) {
+                                     uint64_t logical_batch, int32_t mode,
+                                     const uint64_t *device_key, void *stream) {
   if (model == nullptr || qpos == nullptr || qvel == nullptr || step_count == nullptr ||
       done == nullptr || ep_return == nullptr || ep_length == nullptr)
     return set_invalid("pxr_reset_envs: null argument");
@@ -467,7 +696,8 @@ extern "C" pxr_status pxr_reset_envs(const pxr_model *model, double *qpos, doubl
     return set_unsupported("pxr_reset_envs: 1..16 links");
   reset_kernel<<<blocks_for(batch, 128), 128, 0, (cudaStream_t)stream>>>(
       model->rest_qpos, model->n_links + 2, qpos, qvel, step_count, done, ep_return, ep_length,
-      info_return, info_length, reward, batch, key_hi, key_lo, env_offset, logical_batch, mode);
+      info_return, info_length, reward, batch, key_hi, key_lo, env_offset, logical_batch, mode,
+      device_key);
   return check_launch("reset_kernel");
 }
 

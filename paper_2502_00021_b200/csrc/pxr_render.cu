@@ -139,6 +139,7 @@ struct RenderParams {
   int Hv, Wv;
   int advance;
   uint64_t key_hi, key_lo, env_offset, logical_batch;
+  const uint64_t *device_key;  // key_t read on the device (graph replay), or null
   const uint8_t *done;
   int gray;
   uint8_t *out;
@@ -222,11 +223,13 @@ __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t
   const uint64_t g = p.env_offset + (uint64_t)env;
   out.bias[0] = out.bias[1] = out.bias[2] = 0;
   out.frame_idx = 0;
+  const uint64_t key_hi = p.device_key != nullptr ? __ldg(p.device_key) : p.key_hi;
+  const uint64_t key_lo = p.device_key != nullptr ? __ldg(p.device_key + 1) : p.key_lo;
   if (p.mode == PXR_MODE_COLOR) {
     int16_t b3[3];
     if (p.advance) {
       uint64_t ehi, elo;
-      threefry2x64(p.key_hi, p.key_lo, g, 2, ehi, elo);
+      threefry2x64(key_hi, key_lo, g, 2, ehi, elo);
       color_bias_from_key(ehi, elo, b3);
       for (int c = 0; c < 3; c++) p.color_bias[env * 3 + c] = b3[c];
     } else {
@@ -246,7 +249,7 @@ __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t
       cur = nxt;
       if (p.done != nullptr && p.done[env]) {
         uint64_t rhi, rlo, w0, w1;
-        threefry2x64(p.key_hi, p.key_lo, p.logical_batch + g, 2, rhi, rlo);
+        threefry2x64(key_hi, key_lo, p.logical_batch + g, 2, rhi, rlo);
         threefry2x64(rhi, rlo, 2, 0, w0, w1);
         vid = index_from_word(w0, (uint64_t)p.n_videos);
         cur = 0;
@@ -1419,6 +1422,7 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     p.key_lo = keys->key_lo;
     p.env_offset = keys->env_offset;
     p.logical_batch = keys->logical_batch;
+    p.device_key = keys->device_key;
   }
   p.done = done;
   p.gray = grayscale ? 1 : 0;

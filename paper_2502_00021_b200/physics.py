@@ -252,7 +252,7 @@ def reset_state(spec: ModelSpec, key: Key, batch: int, env_offset: int = 0,
     _native.check(_native.lib().pxr_reset_envs(
         ctypes.byref(dm.c), sys.qpos.data_ptr(), sys.qvel.data_ptr(), sys.step_count.data_ptr(),
         sys.done.data_ptr(), ret.data_ptr(), length.data_ptr(), None, None, None, batch,
-        key.hi, key.lo, env_offset, env_offset + batch, 0, _native.stream_ptr()))
+        key.hi, key.lo, env_offset, env_offset + batch, 0, None, _native.stream_ptr()))
     return sys
 
 

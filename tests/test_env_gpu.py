@@ -206,3 +206,57 @@ class TestStep:
         fg = ~fr.background_mask
         assert fg.any()
         assert torch.equal(ov[fg], on[fg])
+
+
+class TestStepGraph:
+    """StepGraph (policy -> step captured as one CUDA graph, replayed with the
+    step key computed on the device) against the pure ``step`` loop."""
+
+    @pytest.mark.parametrize("name,mode", [("walker_lite", "video"), ("hopper_lite", "color"),
+                                           ("cheetah_lite", "none")])
+    def test_replay_equals_step_loop(self, E, name, mode, tmp_path):
+        import torch
+
+        from paper_2502_00021_b200.bench import ConvStub, conv_stub_forward
+        from paper_2502_00021_b200.bench_support import synthetic_pack
+        from paper_2502_00021_b200.video_pack import save_video_pack
+
+        kw = {}
+        if mode == "video":
+            path = tmp_path / "p.pxvp"
+            save_video_pack(synthetic_pack(), path)
+            kw["video_pack_path"] = str(path)
+        B, T = 24, 120  # long enough for walker falls: resets + video re-draws
+        env, s0, obs0 = _env(E, name, batch=B, seed=3, distractor_mode=mode, **kw)
+        stub = ConvStub.create(84, 84, 3, env.n_joints, seed=0)
+        # reference: the pure step loop
+        s, obs = s0, obs0
+        saw_done = False
+        for _ in range(T):
+            s, out = E.step(env, s, conv_stub_forward(stub, obs))
+            obs = out.obs
+            saw_done |= bool(out.done.any())
+        # graph replay on an independent copy of the initial state
+        g_state = dataclasses.replace(
+            s0, sys=s0.sys.copy(), distractor=s0.distractor.copy(),
+            episode_return=s0.episode_return.clone(), episode_length=s0.episode_length.clone())
+        g = E.StepGraph(env, g_state, obs0.clone(), lambda o: conv_stub_forward(stub, o))
+        g.replay(T - 1)
+        g.replay(1)
+        torch.cuda.synchronize()
+        assert g_state.t == s.t == T
+        assert torch.equal(g.obs, obs)
+        assert torch.equal(g_state.sys.qpos, s.sys.qpos)
+        assert torch.equal(g_state.sys.qvel, s.sys.qvel)
+        assert torch.equal(g_state.sys.step_count, s.sys.step_count)
+        assert torch.equal(g_state.episode_return, s.episode_return)
+        assert torch.equal(g_state.episode_length, s.episode_length)
+        assert torch.equal(g.reward, out.reward)
+        assert torch.equal(g.done.bool(), out.done)
+        assert torch.equal(g.info_length, out.info["episode_length"])
+        for f in ("color_bias", "video_index", "frame_cursor", "direction", "frame_count"):
+            a, b = getattr(g_state.distractor, f, None), getattr(s.distractor, f, None)
+            if a is not None:
+                assert torch.equal(a, b), f
+        if name == "walker_lite":
+            assert saw_done, "the loop should include resets"

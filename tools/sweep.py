@@ -77,23 +77,34 @@ def main():
                 one(i)
             iters_s = max(5, min(100, 50000 // b))
             ms_s = time_events(one, iters_s)
-            rows.append((name, mode, b, b / ms_r * 1e3, ms_r, b / ms_s * 1e3, ms_s))
+            # the same loop as one CUDA graph replay per step (env.StepGraph)
+            g = E.StepGraph(env, box["state"], box["obs"],
+                            lambda o: B.conv_stub_forward(stub, o))
+            g.replay(3)
+            iters_g = max(20, min(1000, 200000 // b))
+            ms_g = time_events(lambda i: g.replay(1), iters_g)
+            rows.append((name, mode, b, b / ms_r * 1e3, ms_r, b / ms_s * 1e3, ms_s,
+                         b / ms_g * 1e3, ms_g))
             print(f"{name:12s} {mode:6s} B={b:6d}  render {b / ms_r * 1e3:12.0f} env-steps/s "
-                  f"({ms_r:.3f} ms)  env_step+policy {b / ms_s * 1e3:12.0f} ({ms_s:.3f} ms)",
-                  flush=True)
+                  f"({ms_r:.3f} ms)  env_step+policy {b / ms_s * 1e3:12.0f} ({ms_s:.3f} ms)  "
+                  f"graphed {b / ms_g * 1e3:12.0f} ({ms_g:.3f} ms)", flush=True)
+            del g
             del env, state, obs, box
             torch.cuda.empty_cache()
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out + ".csv", "w") as f:
-        f.write("model,mode,envs,render_sps,render_ms,env_step_policy_sps,env_step_policy_ms\n")
+        f.write("model,mode,envs,render_sps,render_ms,env_step_policy_sps,env_step_policy_ms,"
+                "graphed_sps,graphed_ms\n")
         for r in rows:
-            f.write(f"{r[0]},{r[1]},{r[2]},{r[3]:.6g},{r[4]:.6g},{r[5]:.6g},{r[6]:.6g}\n")
+            f.write(f"{r[0]},{r[1]},{r[2]},{r[3]:.6g},{r[4]:.6g},{r[5]:.6g},{r[6]:.6g},"
+                    f"{r[7]:.6g},{r[8]:.6g}\n")
     with open(a.out + ".md", "w") as f:
         f.write("| model | distractors | envs | rendered env-steps/s | ms | env step + conv policy, "
-                "env-steps/s | ms |\n|---|---|---|---|---|---|---|\n")
+                "env-steps/s | ms | same, one CUDA graph per step | ms |\n"
+                "|---|---|---|---|---|---|---|---|---|\n")
         for r in rows:
             f.write(f"| {r[0]} | {r[1]} | {r[2]} | {r[3]:,.0f} | {r[4]:.3f} | {r[5]:,.0f} | "
-                    f"{r[6]:.3f} |\n")
+                    f"{r[6]:.3f} | {r[7]:,.0f} | {r[8]:.3f} |\n")
 
 
 if __name__ == "__main__":
