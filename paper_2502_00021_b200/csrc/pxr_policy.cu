@@ -38,7 +38,11 @@ constexpr int kMaxJoints = 32;
 // matrices, LBO = 128 B between the two 8-element K halves, SBO = 256 B
 // between 8-row groups. One thread issues the MMAs; tcgen05.commit arrives
 // on an mbarrier the CTA waits on before reading TMEM.
-constexpr int kTcThreads = 256;
+// Each frame is converted to bf16 ONCE (the 8x8 stride-4 windows overlap, so
+// an im2col straight from the bytes would convert every byte ~4 times) and
+// the A tiles are then built by 16-byte copies from that bf16 frame. One
+// 16-warp CTA per SM (frames + bf16 frame + operands fill shared memory).
+constexpr int kTcThreads = 512;
 constexpr int kTcM = 128, kTcN = 48;
 
 __device__ __forceinline__ uint32_t tc_off(int row, int k, int step_bytes) {
@@ -71,7 +75,8 @@ __device__ __forceinline__ float bf16_val(uint16_t h) {
 
 __global__ void __launch_bounds__(kTcThreads)
 conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W, int C,
-                    const float *__restrict__ conv, float *__restrict__ feat, int bulk) {
+                    const float *__restrict__ conv, float *__restrict__ feat, int bulk,
+                    int use_fb) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int K = kK * kK * C;           // 64 C, a multiple of 16
   const int a_step = (kTcM / 8) * 256;  // bytes per 16-wide K step of A
@@ -81,12 +86,23 @@ conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W
   uint8_t *s_obs0 = s_b + (K / 16) * b_step;
   const int frame = H * W * C;
   const int fstride = (frame + 15) & ~15;
+  const int oh = (H - kK) / kS + 1, ow = (W - kK) / kS + 1, n_pos = oh * ow;
+  int *s_posoff = reinterpret_cast<int *>(s_obs0 + 2 * fstride);  // window start per position
+  uint16_t *s_fb = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(s_posoff) +
+                                                ((4 * n_pos + 15) & ~15));  // bf16 frame (use_fb)
   __shared__ uint64_t s_bar[3];  // frame buffers 0 / 1, MMA completion
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int oh = (H - kK) / kS + 1, ow = (W - kK) / kS + 1, n_pos = oh * ow;
   const float inv = 1.0f / 255.0f;  // float32(1/255), bench.py:101
 
+  // element offset of each output position's window in the frame
+  for (int pos = tid; pos < n_pos; pos += kTcThreads) {
+    const int oy = pos / ow, ox = pos - oy * ow;
+    s_posoff[pos] = (oy * kS * W + ox * kS) * C;
+  }
+  // every 8-element chunk starts 8-byte aligned in the bf16 frame when W C is
+  // a multiple of 4 (window starts are multiples of 4 C elements)
+  const bool chunk_aligned = ((W * C) & 3) == 0;
   // B: the three bf16 splits of every weight, K-major
   for (int i = tid; i < K * kF; i += kTcThreads) {
     const int k = i / kF, f = i - k * kF;
@@ -143,31 +159,62 @@ conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W
       for (int i = tid; i < frame; i += kTcThreads) s_obs[i] = src[i];
       __syncthreads();
     }
+    // the frame as bf16, once (bytes are exact in bf16); frames too large
+    // for a bf16 copy next to the operands are converted per chunk below
+    if (use_fb) {
+      const int n8 = frame >> 3;
+      const uint32_t *src = reinterpret_cast<const uint32_t *>(s_obs);
+      for (int c = tid; c < n8; c += kTcThreads) {
+        const uint32_t lo = src[2 * c], hi = src[2 * c + 1];
+        uint4 v;
+        v.x = bf16x2_of_bytes(lo & 0xffu, (lo >> 8) & 0xffu);
+        v.y = bf16x2_of_bytes((lo >> 16) & 0xffu, lo >> 24);
+        v.z = bf16x2_of_bytes(hi & 0xffu, (hi >> 8) & 0xffu);
+        v.w = bf16x2_of_bytes((hi >> 16) & 0xffu, hi >> 24);
+        reinterpret_cast<uint4 *>(s_fb)[c] = v;
+      }
+      for (int i = (n8 << 3) + tid; i < frame; i += kTcThreads)
+        s_fb[i] = (uint16_t)(bf16x2_of_bytes(s_obs[i], 0u) & 0xffffu);
+    }
+    __syncthreads();
     float *fe = feat + env * (int64_t)(n_pos * kF);
     for (int m0 = 0; m0 < n_pos; m0 += kTcM) {
-      // A: im2col rows of this tile; item (row, ky) = 8 C consecutive bytes
+      // A: im2col rows of this tile; item (row, ky) = 8 C consecutive bytes.
+      // Consecutive lanes take consecutive rows: each quarter-warp's 16-B
+      // stores then fill one 128-B line of the K-major layout (no bank
+      // conflicts) and the source words are 12 B apart (conflict-free too).
+      static_assert(kTcM == 128, "row = item & 127");
       for (int item = tid; item < kTcM * kK; item += kTcThreads) {
-        const int row = item >> 3, ky = item & 7, pos = m0 + row;
+        const int row = item & (kTcM - 1), ky = item >> 7, pos = m0 + row;
         if (pos >= n_pos) continue;  // rows past the end are computed and dropped
-        const int oy = pos / ow, ox = pos - oy * ow;
-        const int boff = ((oy * kS + ky) * W + ox * kS) * C;
-        PXR_DCHECK(oy * kS + ky < H && ox * kS + kK <= W && boff + 8 * C <= frame);
-        const uint8_t *src = s_obs + boff;
+        const int e0 = s_posoff[pos] + ky * W * C;
+        PXR_DCHECK(e0 + 8 * C <= frame);
         for (int ch = 0; ch < C; ch++) {  // 8-element K chunks
-          uint32_t lo, hi;
-          if (((boff + 8 * ch) & 3) == 0) {  // two aligned words
-            lo = *reinterpret_cast<const uint32_t *>(src + 8 * ch);
-            hi = *reinterpret_cast<const uint32_t *>(src + 8 * ch + 4);
-          } else {
-            const uint8_t *b8 = src + 8 * ch;
-            lo = b8[0] | (b8[1] << 8) | (b8[2] << 16) | ((uint32_t)b8[3] << 24);
-            hi = b8[4] | (b8[5] << 8) | (b8[6] << 16) | ((uint32_t)b8[7] << 24);
-          }
+          const int e = e0 + 8 * ch;
           uint4 v;
-          v.x = bf16x2_of_bytes(lo & 0xffu, (lo >> 8) & 0xffu);
-          v.y = bf16x2_of_bytes((lo >> 16) & 0xffu, lo >> 24);
-          v.z = bf16x2_of_bytes(hi & 0xffu, (hi >> 8) & 0xffu);
-          v.w = bf16x2_of_bytes((hi >> 16) & 0xffu, hi >> 24);
+          if (!use_fb) {  // straight from the bytes
+            const uint8_t *b8 = s_obs + e;
+            uint32_t lo, hi;
+            if ((e & 3) == 0) {
+              lo = *reinterpret_cast<const uint32_t *>(b8);
+              hi = *reinterpret_cast<const uint32_t *>(b8 + 4);
+            } else {
+              lo = b8[0] | (b8[1] << 8) | (b8[2] << 16) | ((uint32_t)b8[3] << 24);
+              hi = b8[4] | (b8[5] << 8) | (b8[6] << 16) | ((uint32_t)b8[7] << 24);
+            }
+            v.x = bf16x2_of_bytes(lo & 0xffu, (lo >> 8) & 0xffu);
+            v.y = bf16x2_of_bytes((lo >> 16) & 0xffu, lo >> 24);
+            v.z = bf16x2_of_bytes(hi & 0xffu, (hi >> 8) & 0xffu);
+            v.w = bf16x2_of_bytes((hi >> 16) & 0xffu, hi >> 24);
+          } else if (chunk_aligned) {
+            const uint2 a = *reinterpret_cast<const uint2 *>(s_fb + e);
+            const uint2 b = *reinterpret_cast<const uint2 *>(s_fb + e + 4);
+            v = make_uint4(a.x, a.y, b.x, b.y);
+          } else {
+            const uint16_t *h = s_fb + e;
+            v = make_uint4((uint32_t)h[0] | ((uint32_t)h[1] << 16), (uint32_t)h[2] | ((uint32_t)h[3] << 16),
+                           (uint32_t)h[4] | ((uint32_t)h[5] << 16), (uint32_t)h[6] | ((uint32_t)h[7] << 16));
+          }
           PXR_DCHECK(tc_off(row, ky * 8 * C + 8 * ch, a_step) + 16u <= (uint32_t)((K / 16) * a_step));
           *reinterpret_cast<uint4 *>(s_a + tc_off(row, ky * 8 * C + 8 * ch, a_step)) = v;
         }
@@ -191,30 +238,27 @@ conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W
       mma_phase ^= 1u;
       asm volatile("tcgen05.fence::after_thread_sync;");
       // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (its rows) and
-      // filters 8 (w / 4) .. +7 of each split
-      const int q = warp & 3, fh = (warp >> 2) * 8;
+      // filters 4 (w / 4) .. +3 of each split
+      static_assert(kTcThreads == 512, "16 warps: 4 lane quarters x 4 filter quarters");
+      const int q = warp & 3, fh = (warp >> 2) * 4;
       const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16);
-      uint32_t d[3][8];
+      uint32_t d[3][4];
 #pragma unroll
       for (int sp = 0; sp < 3; sp++)
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-            : "=r"(d[sp][0]), "=r"(d[sp][1]), "=r"(d[sp][2]), "=r"(d[sp][3]), "=r"(d[sp][4]),
-              "=r"(d[sp][5]), "=r"(d[sp][6]), "=r"(d[sp][7])
-            : "r"(ta + (uint32_t)(sp * 16 + fh)));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(d[sp][0]), "=r"(d[sp][1]), "=r"(d[sp][2]), "=r"(d[sp][3])
+                     : "r"(ta + (uint32_t)(sp * 16 + fh)));
       asm volatile("tcgen05.wait::ld.sync.aligned;");
       const int pos = m0 + 32 * q + lane;
       if (pos < n_pos) {
-        float o[8];
+        float o[4];
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
+        for (int i = 0; i < 4; i++) {
           const float v = (__uint_as_float(d[0][i]) + __uint_as_float(d[1][i]) +
                            __uint_as_float(d[2][i])) * inv;
           o[i] = v > 0.0f ? v : 0.0f;  // ReLU
         }
-        float4 *dst = reinterpret_cast<float4 *>(fe + pos * kF + fh);
-        dst[0] = make_float4(o[0], o[1], o[2], o[3]);
-        dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+        *reinterpret_cast<float4 *>(fe + pos * kF + fh) = make_float4(o[0], o[1], o[2], o[3]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncthreads();  // TMEM and A are reused by the next tile
@@ -229,38 +273,52 @@ conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W
 constexpr int kProjEnvs = 8;
 constexpr int kProjTile = 256;  // proj rows per shared-memory tile
 
+// JP = J rounded up to a multiple of 4: the staged proj rows are padded with
+// zeros to JP floats so each lane reads its row with 128-bit loads (rows
+// 16 B-aligned; 8 consecutive rows of a quarter-warp hit distinct banks for
+// every JP used) and the FMA chain of each real output j < J is exactly the
+// unpadded one.
+template <int JP>
 __global__ void __launch_bounds__(kProjEnvs * 32)
 conv_proj_kernel(const float *__restrict__ feat, int64_t batch, int K,
                  const float *__restrict__ proj, int J, double *__restrict__ out) {
   extern __shared__ __align__(16) unsigned char sm[];
-  float *s_p = reinterpret_cast<float *>(sm);  // kProjTile x J
+  float *s_p = reinterpret_cast<float *>(sm);  // kProjTile x JP
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  PXR_DCHECK(J >= 1 && J <= JP && JP <= kMaxJoints);
   for (int64_t e0 = (int64_t)blockIdx.x * kProjEnvs; e0 < batch;
        e0 += (int64_t)gridDim.x * kProjEnvs) {
     const int64_t env = e0 + warp;
     const float *fr = feat + env * (int64_t)K;
-    PXR_DCHECK(J >= 1 && J <= kMaxJoints);
-    float pacc[kMaxJoints];
+    float pacc[JP];
 #pragma unroll
-    for (int j = 0; j < kMaxJoints; j++) pacc[j] = 0.0f;
+    for (int j = 0; j < JP; j++) pacc[j] = 0.0f;
     for (int k0 = 0; k0 < K; k0 += kProjTile) {
       const int kn = min(kProjTile, K - k0);
       __syncthreads();  // previous tile no longer read
-      for (int i = tid; i < kn * J; i += kProjEnvs * 32) s_p[i] = __ldg(proj + (int64_t)k0 * J + i);
+      for (int i = tid; i < kn * JP; i += kProjEnvs * 32) {
+        const int r = i / JP, j = i - r * JP;
+        s_p[i] = j < J ? __ldg(proj + (int64_t)(k0 + r) * J + j) : 0.0f;
+      }
       __syncthreads();
       if (env < batch) {
         for (int kk = lane; kk < kn; kk += 32) {
           const float v = __ldg(fr + k0 + kk);
-          const float *pr = s_p + kk * J;
+          const float4 *pr = reinterpret_cast<const float4 *>(s_p + kk * JP);
 #pragma unroll
-          for (int j = 0; j < kMaxJoints; j++)
-            if (j < J) pacc[j] = __fmaf_rn(v, pr[j], pacc[j]);
+          for (int j4 = 0; j4 < JP / 4; j4++) {
+            const float4 w = pr[j4];
+            pacc[4 * j4 + 0] = __fmaf_rn(v, w.x, pacc[4 * j4 + 0]);
+            pacc[4 * j4 + 1] = __fmaf_rn(v, w.y, pacc[4 * j4 + 1]);
+            pacc[4 * j4 + 2] = __fmaf_rn(v, w.z, pacc[4 * j4 + 2]);
+            pacc[4 * j4 + 3] = __fmaf_rn(v, w.w, pacc[4 * j4 + 3]);
+          }
         }
       }
     }
     if (env < batch) {
 #pragma unroll
-      for (int j = 0; j < kMaxJoints; j++) {
+      for (int j = 0; j < JP; j++) {
         if (j >= J) break;
         float v = pacc[j];
 #pragma unroll
@@ -290,14 +348,19 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   const int frame = height * width * channels;
   const int bulk = (frame % 16 == 0) && ((reinterpret_cast<uintptr_t>(obs) & 15) == 0);
   const int Kc = kK * kK * channels;
-  const int smem = (Kc / 16) * ((kTcM / 8) * 256) + (Kc / 16) * ((kTcN / 8) * 256) +
+  const int n_pos = ((height - kK) / kS + 1) * ((width - kK) / kS + 1);
+  const int base = (Kc / 16) * ((kTcM / 8) * 256) + (Kc / 16) * ((kTcN / 8) * 256) +
                    2 * ((frame + 15) & ~15);
+  // the bf16 frame copy when it fits, else the per-chunk conversion
+  const int with_table = base + ((4 * n_pos + 15) & ~15);
+  const int use_fb = with_table + ((2 * frame + 15) & ~15) <= 220 * 1024;
+  const int smem = use_fb ? with_table + ((2 * frame + 15) & ~15) : with_table;
   if (smem > 220 * 1024) return set_unsupported("observation too large for the policy kernel");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaFuncSetAttribute(conv_feat_tc_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
-  // the full shared-memory carveout, so two CTAs (frames + operands) share an SM
+  // the full shared-memory carveout (frames + bf16 frame + operands)
   e = cudaFuncSetAttribute(conv_feat_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                            100);
   if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
@@ -314,17 +377,29 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   int64_t cap = (int64_t)sms * per_sm;
   int grid = (int)(batch < cap ? batch : cap);
   conv_feat_tc_kernel<<<grid, kTcThreads, smem, st>>>(obs, batch, height, width, channels, conv,
-                                                      workspace, bulk);
+                                                      workspace, bulk, use_fb);
   pxr_status s = check_launch("conv_feat_tc_kernel");
   if (s != PXR_OK) return s;
   const int K = ((height - kK) / kS + 1) * ((width - kK) / kS + 1) * kF;
-  const int psmem = kProjTile * n_joints * (int)sizeof(float);
+  const int jp = (n_joints + 3) & ~3;
+  const int psmem = kProjTile * jp * (int)sizeof(float);
+  void (*pk)(const float *, int64_t, int, const float *, int, double *) = nullptr;
+  switch (jp) {
+    case 4: pk = conv_proj_kernel<4>; break;
+    case 8: pk = conv_proj_kernel<8>; break;
+    case 12: pk = conv_proj_kernel<12>; break;
+    case 16: pk = conv_proj_kernel<16>; break;
+    case 20: pk = conv_proj_kernel<20>; break;
+    case 24: pk = conv_proj_kernel<24>; break;
+    case 28: pk = conv_proj_kernel<28>; break;
+    default: pk = conv_proj_kernel<32>; break;
+  }
   per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_proj_kernel, kProjEnvs * 32, psmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk, kProjEnvs * 32, psmem);
   if (per_sm < 1) per_sm = 1;
   cap = (int64_t)sms * per_sm;
   const int64_t groups = (batch + kProjEnvs - 1) / kProjEnvs;
   grid = (int)(groups < cap ? groups : cap);
-  conv_proj_kernel<<<grid, kProjEnvs * 32, psmem, st>>>(workspace, batch, K, proj, n_joints, out);
+  pk<<<grid, kProjEnvs * 32, psmem, st>>>(workspace, batch, K, proj, n_joints, out);
   return check_launch("conv_proj_kernel");
 }

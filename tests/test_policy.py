@@ -127,6 +127,14 @@ class TestConvStubGPU:
         got = B.conv_stub_forward(stub, obs)
         assert float((got - want).abs().max()) < 1e-5
 
+    def test_large_frames_convert_per_chunk(self, B):
+        """Frames too large for the kernel's bf16 frame copy (140x140 RGB)
+        take the per-chunk conversion path; same results."""
+        stub = B.ConvStub.create(140, 140, 3, 5, seed=2)
+        obs = np.random.default_rng(4).integers(0, 256, (3, 140, 140, 3), dtype=np.uint8)
+        got = B.conv_stub_forward(stub, obs)
+        assert np.max(np.abs(got - f64_forward(stub.conv, stub.proj, obs))) < 1e-5
+
     def test_zero_weights_and_shape_errors(self, B):
         stub = B.ConvStub.create(32, 32, 3, 4, seed=0)
         zero = dataclasses.replace(stub, conv=np.zeros_like(stub.conv),
