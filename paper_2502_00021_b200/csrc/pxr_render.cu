@@ -71,8 +71,10 @@ constexpr int kRowCap = 2560;   // bbox rows (>= spans) per raster round (raised
 constexpr int kFragCap = 1536;  // fragment list capacity (overflow: recompute)
 constexpr uint32_t kDecBit = 0x80000000u;
 // debug workload counters per env: live triangles, bbox-row units, non-empty
-// spans, candidate pixels, covered fragments, raster rounds, overflow rounds
-constexpr int kStats = 7;
+// spans, candidate pixels, covered fragments, raster rounds, overflow rounds,
+// live triangles that cover no pixel centre, their bbox-row units, those of
+// them with a single bbox row
+constexpr int kStats = 10;
 #ifdef PXR_CHECKED
 constexpr bool kWithStats = true;  // counters only in the checked build
 #else
@@ -1172,9 +1174,25 @@ render_step_kernel(const RenderParams p) {
 
         // exact sequential-order resolve (see the file header)
         const int n_frag = es.n_frag;
-        if (kWithStats && p.stats != nullptr && tid == 0) {
-          es.st[4] += n_frag;
-          es.st[6] += n_frag > p.frag_limit;
+        if (kWithStats && p.stats != nullptr) {
+          if (tid == 0) {
+            es.st[4] += n_frag;
+            es.st[6] += n_frag > p.frag_limit;
+          }
+          // triangles with at least one covered pixel: bit 15 of their flags
+          // (only eval_exact reads the flags, and it has run)
+          for (int i = tid; i < min(n_frag, p.frag_limit); i += kThreads)
+            atomicOr(reinterpret_cast<uint32_t *>(&s_rec[s_frag[i].y >> 20]) + 11, 0x80000000u);
+          __syncthreads();
+          for (int li = tid; li < n_round; li += kThreads) {
+            if (!(s_rec[li].flags & 0x8000u)) {
+              const int rows = (int)(s_lrp[r0 + li + 1] - s_lrp[r0 + li]);
+              atomicAdd(&es.st[7], 1);
+              atomicAdd(&es.st[8], rows);
+              if (rows == 1) atomicAdd(&es.st[9], 1);
+            }
+          }
+          __syncthreads();
         }
         if (n_frag <= p.frag_limit) {
           for (int i = tid; i < n_frag; i += kThreads) {
