@@ -229,8 +229,12 @@ def run_ours(args, world, rank, local):
     if not args.no_e2e:
         e2e = run_e2e(args, w, dev, world, rank)
 
+    # ---- determinism + shard-slice check, per-rank digest (untimed) --------
+    mism, digest = verify_rank(args, w, shard, pack, dev)
+
     # ---- final stats gather (NCCL): the only collective --------------------
-    stats = gather_stats({"env_steps": B * args.steps, "ms": ms, "mismatches": 0})
+    stats = gather_stats({"env_steps": B * args.steps, "ms": ms, "mismatches": mism,
+                          "digest_lo": digest & 0xFFFFFFFF, "digest_hi": digest >> 32})
     agg = aggregate(stats)
     if world > 1:
         tdist.destroy_process_group()
@@ -287,13 +291,55 @@ def run_ours(args, world, rank, local):
         },
         "gpu_launches": args.steps,
         "stats_gather": {"ranks": len(stats), "env_steps": agg["env_steps"],
-                         "ms_max": agg["ms_max"]},
+                         "ms_max": agg["ms_max"], "mismatches": agg["mismatches"],
+                         "digests": [f"{(int(r['digest_hi']) << 32) | int(r['digest_lo']):016x}"
+                                     for r in stats],
+                         "check": "per rank: the same step rendered twice from one saved "
+                                  "distractor state, and a 64-env slice rendered as its own "
+                                  "batch (env_offset / logical_batch impersonation), compared "
+                                  "byte for byte with the full batch; digest = first 64 bits "
+                                  "of SHA-256 of the rank's obs"},
         "e2e": e2e,
         "clocks": clocks,
     }
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(args, w, seconds=args.cpu_seconds)
     return line
+
+
+def verify_rank(args, w, shard, pack, dev):
+    """Untimed correctness check of this rank's shard (no oracle): one step
+    rendered twice from the same saved distractor state must agree byte for
+    byte (catches races), and the first min(64, B) envs rendered as their
+    own batch -- the slice impersonation of SURVEY 8(e): keys and poses come
+    from the global env index -- must equal those rows of the full batch.
+    Returns (mismatching bytes, first 64 bits of SHA-256 of the obs)."""
+    import hashlib
+
+    import torch
+
+    from paper_2502_00021_b200.bench_support import Workload
+
+    T = 7919  # any step index
+    poses = w.poses(T).clone()
+    d0 = w.dist.copy()
+    a, _ = w.render(poses, T, out_obs=torch.empty_like(w.obs))
+    fields = ("color_bias", "video_index", "frame_cursor", "direction", "frame_count")
+    for f in fields:  # back to the saved state, same step again
+        getattr(w.dist, f).copy_(getattr(d0, f))
+    b, _ = w.render(poses, T, out_obs=torch.empty_like(w.obs))
+    m = min(64, w.batch)
+    ws = Workload(args.model, m, args.mode, seed=0, env_offset=shard.env_offset,
+                  logical_batch=shard.logical_batch, grayscale=args.grayscale, pack=pack,
+                  device=dev)
+    for f in fields:
+        src = getattr(d0, f)
+        if src.numel():
+            getattr(ws.dist, f).copy_(src[:m])
+    c, _ = ws.render(ws.poses(T).clone(), T)
+    mism = int((a != b).sum().item()) + int((a[:m] != c).sum().item())
+    digest = int(hashlib.sha256(a.cpu().numpy().tobytes()).hexdigest()[:16], 16)
+    return mism, digest
 
 
 def run_e2e(args, w, dev, world, rank):
