@@ -212,23 +212,26 @@ class TestStepGraph:
     """StepGraph (policy -> step captured as one CUDA graph, replayed with the
     step key computed on the device) against the pure ``step`` loop."""
 
-    @pytest.mark.parametrize("name,mode", [("walker_lite", "video"), ("hopper_lite", "color"),
-                                           ("cheetah_lite", "none")])
-    def test_replay_equals_step_loop(self, E, name, mode, tmp_path):
+    @pytest.mark.parametrize("name,mode,extra", [
+        ("walker_lite", "video", {}), ("hopper_lite", "color", {}), ("cheetah_lite", "none", {}),
+        ("walker_lite", "video", {"observation": "grayscale", "logical_batch": 96,
+                                  "env_offset": 48}),
+    ])
+    def test_replay_equals_step_loop(self, E, name, mode, extra, tmp_path):
         import torch
 
         from paper_2502_00021_b200.bench import ConvStub, conv_stub_forward
         from paper_2502_00021_b200.bench_support import synthetic_pack
         from paper_2502_00021_b200.video_pack import save_video_pack
 
-        kw = {}
+        kw = dict(extra)
         if mode == "video":
             path = tmp_path / "p.pxvp"
             save_video_pack(synthetic_pack(), path)
             kw["video_pack_path"] = str(path)
         B, T = 24, 120  # long enough for walker falls: resets + video re-draws
         env, s0, obs0 = _env(E, name, batch=B, seed=3, distractor_mode=mode, **kw)
-        stub = ConvStub.create(84, 84, 3, env.n_joints, seed=0)
+        stub = ConvStub.create(84, 84, int(obs0.shape[-1]), env.n_joints, seed=0)
         # reference: the pure step loop
         s, obs = s0, obs0
         saw_done = False
