@@ -80,6 +80,15 @@ def read_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def ncu_entry(workload_tag):
+    """The committed ncu capture summary of a workload (profiles/ncu_summary.json)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get("workloads", {}).get(workload_tag)
+    except Exception:
+        return None
+
+
 def ncu_traffic(workload_tag):
     """Per-launch DRAM bytes of the fused kernel from the committed ncu
     capture summary (profiles/ncu_summary.json), if it matches."""
@@ -251,6 +260,21 @@ def run_ours(args, world, rank, local):
     tag = (f"{args.model}-{args.mode}-{B}{'-gray' if args.grayscale else ''}"
            f"{f'-pack{args.pack_videos}' if args.pack_videos != 4 else ''}")
     traffic = ncu_traffic(tag)
+    # what does bound it: warp instructions per env (ncu capture of this
+    # workload) x env-steps/s (this run) / (SMs x 4 schedulers x SM clock)
+    issue = None
+    ent = ncu_entry(tag)
+    if ent and ent.get("warp_instructions_per_env") and clocks and clocks.get("sm_mhz"):
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        ipe = float(ent["warp_instructions_per_env"])
+        rate = ipe * (B / per_launch_s)
+        peak_i = sms * 4 * clocks["sm_mhz"] * 1e6
+        issue = {"bound": "issue", "warp_instructions_per_env": ipe,
+                 "achieved_warp_instr_per_s": rate, "peak_warp_instr_per_s": peak_i,
+                 "frac": rate / peak_i,
+                 "note": "instructions per env from the committed ncu capture; the rate from "
+                         "this run's device time and sampled SM clock (4 issue slots per SM "
+                         "per cycle)"}
     line = {
         "metric": METRIC,
         "value": value,
@@ -289,6 +313,7 @@ def run_ours(args, world, rank, local):
             "peak_source": peak_src,
             "kernel": "render_step_kernel",
         },
+        "issue": issue,
         "gpu_launches": args.steps,
         "stats_gather": {"ranks": len(stats), "env_steps": agg["env_steps"],
                          "ms_max": agg["ms_max"], "mismatches": agg["mismatches"],
