@@ -318,16 +318,29 @@ struct WarpPhys {
       voz[kMaxL], fex[kMaxL], fez[kMaxL], tex[kMaxL];
 };
 
+// kLanes = 32: one warp per env; kLanes = 16: two envs per warp (needs
+// nd < 16: one lane per dof plus the bias lane), twice the envs in flight for
+// the same per-env latency chain -- the middle batch range.
+template <int kLanes>
 __global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(StepArgs a) {
-  __shared__ WarpPhys s_env[kPhysWarps];
+  constexpr int kPer = 32 / kLanes;  // envs per warp
+  __shared__ WarpPhys s_env[kPhysWarps * kPer];
   const Model &m = a.m;
   const int nl = m.nl, nd = nl + 2, nj = nd - 3;
   const int active0 = a.fixed_root ? 3 : 0;
-  const int lane = threadIdx.x & 31;
-  WarpPhys &S = s_env[threadIdx.x >> 5];
-  PXR_DCHECK(nl >= 1 && nl <= kMaxL && nd <= kMaxD && nd < 32 && m.parent[0] < 0);
-  for (int64_t b = (int64_t)blockIdx.x * kPhysWarps + (threadIdx.x >> 5); b < a.batch;
-       b += (int64_t)gridDim.x * kPhysWarps) {
+  const int lane = threadIdx.x & (kLanes - 1);
+  const int slot = threadIdx.x / kLanes;
+  WarpPhys &S = s_env[slot];
+  PXR_DCHECK(nl >= 1 && nl <= kMaxL && nd <= kMaxD && nd < kLanes && m.parent[0] < 0);
+  // every lane of a block runs the same iterations (the warp syncs span the
+  // envs sharing a warp); a slot past the batch recomputes env 0 unstored
+  for (int64_t base = (int64_t)blockIdx.x * (kPhysWarps * kPer); base < a.batch;
+       base += (int64_t)gridDim.x * (kPhysWarps * kPer)) {
+    // (a warp with no env left skips -- warp-uniform; otherwise its lanes
+    // stay in lockstep)
+    if (base + (int64_t)(threadIdx.x >> 5) * kPer >= a.batch) continue;
+    const bool valid = base + slot < a.batch;
+    const int64_t b = valid ? base + slot : 0;
     double *q = a.qpos + b * nd, *qd = a.qvel + b * nd;
     const double *act = a.actions + b * nj;
     if (lane < nd) {
@@ -415,14 +428,14 @@ __global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(Step
         S.tau[lane] = t;
       }
       __syncwarp();
-      // RNEA bias (lane 31) and the mass-matrix columns (lane j)
-      if (lane == 31 || (lane >= active0 && lane < nd)) {
+      // RNEA bias (last lane) and the mass-matrix columns (lane j)
+      if (lane == kLanes - 1 || (lane >= active0 && lane < nd)) {
         double zeros[kMaxD], vec[kMaxD], col[kMaxD];
         for (int d = 0; d < nd; d++) {
           zeros[d] = 0.0;
           vec[d] = d == lane ? 1.0 : 0.0;
         }
-        if (lane == 31) {
+        if (lane == kLanes - 1) {
           rnea(m, S.qb, S.qdb, zeros, S.ct, S.st, GRAVITY, S.fex, S.fez, S.tex, true, col);
           for (int d = 0; d < nd; d++) S.bias[d] = col[d];
         } else {
@@ -474,7 +487,7 @@ __global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(Step
       }
       __syncwarp();
     }
-    if (lane == 0) {
+    if (lane == 0 && valid) {
       // non-finite guard (physics.py:401-412)
       bool finite = true;
       for (int d = 0; d < nd; d++) {
@@ -624,6 +637,10 @@ __global__ void fk_env_kernel(const double *qpos, const int32_t *parent, const d
 // measured crossover (tools/phys_bench.py, B200): warp-per-env is 1.6-2.4x
 // faster up to ~1-2k envs, one thread per env wins from ~4k on
 constexpr int64_t kWarpEnvMax = 2048;
+// half a warp per env (nd < 16) beats a whole warp at every batch and one
+// thread per env up to ~4k envs for the larger models (Humanoid 0.61 vs
+// 0.76 ms at 4096), ~2-3k for the smaller ones
+constexpr int64_t kHalfEnvMaxLarge = 4096, kHalfEnvMaxSmall = 2048;
 
 static inline unsigned blocks_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
@@ -665,14 +682,23 @@ extern "C" pxr_status pxr_physics_step(const pxr_model *model, double *qpos, dou
   a.forward_weight = model->forward_weight;
   a.ctrl_cost = model->ctrl_cost;
   a.ep_len = model->episode_length;
-  // one warp per env up to kWarpEnvMax envs (latency-bound range), one
-  // thread per env above (throughput); PXR_DEBUG_PHYS=warp|thread forces one
+  // half a warp per env (nd < 16) or a whole warp (larger models) in the
+  // latency-bound range, one thread per env above
+  // (throughput); PXR_DEBUG_PHYS=warp|half|thread forces one
   const char *force = getenv("PXR_DEBUG_PHYS");
-  bool warp = batch <= kWarpEnvMax;
-  if (force != nullptr) warp = force[0] == 'w';
-  if (warp) {
-    physics_step_warp_kernel<<<blocks_for((batch + kPhysWarps - 1) / kPhysWarps, 1),
-                               kPhysWarps * 32, 0, (cudaStream_t)stream>>>(a);
+  const int nd = model->n_links + 2;
+  const int64_t half_max = nd >= 12 ? kHalfEnvMaxLarge : kHalfEnvMaxSmall;
+  char kind = nd < 16 && batch <= half_max ? 'h' : (batch <= kWarpEnvMax ? 'w' : 't');
+  if (force != nullptr) kind = force[0];
+  if (kind == 'h' && nd >= 16) kind = 'w';
+  if (kind == 'w') {
+    physics_step_warp_kernel<32><<<blocks_for((batch + kPhysWarps - 1) / kPhysWarps, 1),
+                                   kPhysWarps * 32, 0, (cudaStream_t)stream>>>(a);
+    return check_launch("physics_step_warp_kernel");
+  }
+  if (kind == 'h') {
+    physics_step_warp_kernel<16><<<blocks_for((batch + 2 * kPhysWarps - 1) / (2 * kPhysWarps), 1),
+                                   kPhysWarps * 32, 0, (cudaStream_t)stream>>>(a);
     return check_launch("physics_step_warp_kernel");
   }
   physics_step_kernel<<<blocks_for(batch, 64), 64, 0, (cudaStream_t)stream>>>(a);
