@@ -2,8 +2,10 @@
 // device -- SURVEY.md 8(f) row 1 ("GPU physics + FK + reset"), so that the
 // reference's Env.step() runs without a host round trip.
 //
-// One thread per env, f64, mirroring the reference's numba kernels
-// operation by operation (all under /root/reference/pkg/src/pixelctrl/):
+// f64, mirroring the reference's numba kernels operation by operation (all
+// under /root/reference/pkg/src/pixelctrl/), as one thread per env (large
+// batches) or 32 / 16 / 8 lanes per env (the latency-bound smaller batches;
+// same arithmetic per element, bit-identical results):
 //   _kinematics_pass  physics.py:144-163
 //   _rnea             physics.py:166-238
 //   _solve_spd        physics.py:241-269
@@ -309,7 +311,6 @@ __global__ void physics_step_kernel(StepArgs a) {
 // column by column with its rows in parallel. Every element is computed by
 // the same operations in the same order as physics_step_kernel, so the two
 // kernels agree bit for bit (tests/test_physics_api.py).
-constexpr int kPhysWarps = 4;  // envs per block
 
 struct WarpPhys {
   double qb[kMaxD], qdb[kMaxD], q0[kMaxD], tau[kMaxD], bias[kMaxD], rhs[kMaxD], qdd[kMaxD];
@@ -318,24 +319,25 @@ struct WarpPhys {
       voz[kMaxL], fex[kMaxL], fez[kMaxL], tex[kMaxL];
 };
 
-// kLanes = 32: one warp per env; kLanes = 16: two envs per warp (needs
-// nd < 16: one lane per dof plus the bias lane), twice the envs in flight for
-// the same per-env latency chain -- the middle batch range.
+// kLanes lanes per env (32, 16 or 8: 1, 2 or 4 envs per warp); per-link /
+// per-dof / per-column work is strided over the env's lanes. Fewer lanes per
+// env: more envs in flight, longer per-env chain -- see the dispatch below.
 template <int kLanes>
-__global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(StepArgs a) {
-  constexpr int kPer = 32 / kLanes;  // envs per warp
-  __shared__ WarpPhys s_env[kPhysWarps * kPer];
+__global__ void __launch_bounds__(kLanes == 8 ? 64 : 128) physics_step_warp_kernel(StepArgs a) {
+  constexpr int kPer = 32 / kLanes;                  // envs per warp
+  constexpr int kWarpsPB = kLanes == 8 ? 2 : 4;      // warps per block
+  __shared__ WarpPhys s_env[kWarpsPB * kPer];
   const Model &m = a.m;
   const int nl = m.nl, nd = nl + 2, nj = nd - 3;
   const int active0 = a.fixed_root ? 3 : 0;
   const int lane = threadIdx.x & (kLanes - 1);
   const int slot = threadIdx.x / kLanes;
   WarpPhys &S = s_env[slot];
-  PXR_DCHECK(nl >= 1 && nl <= kMaxL && nd <= kMaxD && nd < kLanes && m.parent[0] < 0);
+  PXR_DCHECK(nl >= 1 && nl <= kMaxL && nd <= kMaxD && m.parent[0] < 0);
   // every lane of a block runs the same iterations (the warp syncs span the
   // envs sharing a warp); a slot past the batch recomputes env 0 unstored
-  for (int64_t base = (int64_t)blockIdx.x * (kPhysWarps * kPer); base < a.batch;
-       base += (int64_t)gridDim.x * (kPhysWarps * kPer)) {
+  for (int64_t base = (int64_t)blockIdx.x * (kWarpsPB * kPer); base < a.batch;
+       base += (int64_t)gridDim.x * (kWarpsPB * kPer)) {
     // (a warp with no env left skips -- warp-uniform; otherwise its lanes
     // stay in lockstep)
     if (base + (int64_t)(threadIdx.x >> 5) * kPer >= a.batch) continue;
@@ -343,10 +345,10 @@ __global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(Step
     const int64_t b = valid ? base + slot : 0;
     double *q = a.qpos + b * nd, *qd = a.qvel + b * nd;
     const double *act = a.actions + b * nj;
-    if (lane < nd) {
-      S.qb[lane] = q[lane];
-      S.qdb[lane] = qd[lane];
-      S.q0[lane] = q[lane];
+    for (int d = lane; d < nd; d += kLanes) {
+      S.qb[d] = q[d];
+      S.qdb[d] = qd[d];
+      S.q0[d] = q[d];
     }
     __syncwarp();
     const double x_before = S.qb[0];
@@ -358,9 +360,9 @@ __global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(Step
         for (int i = 1; i < nl; i++) S.theta[i] = S.theta[m.parent[i]] + S.qb[3 + i - 1];
       }
       __syncwarp();
-      if (lane < nl) {
-        S.ct[lane] = cos(S.theta[lane]);
-        S.st[lane] = sin(S.theta[lane]);
+      for (int i = lane; i < nl; i += kLanes) {
+        S.ct[i] = cos(S.theta[i]);
+        S.st[i] = sin(S.theta[i]);
       }
       __syncwarp();
       if (lane == 0) {
@@ -380,8 +382,7 @@ __global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(Step
       }
       __syncwarp();
       // ground contact at both capsule ends (physics.py:321-353), one link per lane
-      if (lane < nl) {
-        const int i = lane;
+      for (int i = lane; i < nl; i += kLanes) {
         const double c = S.ct[i], s = S.st[i];
         double fx = 0.0, fz = 0.0, tx = 0.0;
         for (int end = 0; end < 2; end++) {
@@ -412,10 +413,10 @@ __global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(Step
         S.tex[i] = tx;
       }
       // actuation + joint-limit penalty (physics.py:355-370), one dof per lane
-      if (lane < nd) {
+      for (int d = lane; d < nd; d += kLanes) {
         double t = 0.0;
-        if (lane >= 3) {
-          const int j = lane - 3;
+        if (d >= 3) {
+          const int j = d - 3;
           double av = act[j];
           if (av > 1.0) av = 1.0;
           else if (av < -1.0) av = -1.0;
@@ -425,26 +426,27 @@ __global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(Step
           else if (qj > m.limit_hi[j]) t -= LIMIT_SPRING * (qj - m.limit_hi[j]) + LIMIT_DAMPING * S.qdb[3 + j];
           t -= JOINT_DAMPING * S.qdb[3 + j];
         }
-        S.tau[lane] = t;
+        S.tau[d] = t;
       }
       __syncwarp();
-      // RNEA bias (last lane) and the mass-matrix columns (lane j)
-      if (lane == kLanes - 1 || (lane >= active0 && lane < nd)) {
+      // the mass-matrix columns (item j) and the RNEA bias (item nd)
+      for (int it = lane; it <= nd; it += kLanes) {
+        if (it < active0) continue;
         double zeros[kMaxD], vec[kMaxD], col[kMaxD];
         for (int d = 0; d < nd; d++) {
           zeros[d] = 0.0;
-          vec[d] = d == lane ? 1.0 : 0.0;
+          vec[d] = d == it ? 1.0 : 0.0;
         }
-        if (lane == kLanes - 1) {
+        if (it == nd) {
           rnea(m, S.qb, S.qdb, zeros, S.ct, S.st, GRAVITY, S.fex, S.fez, S.tex, true, col);
           for (int d = 0; d < nd; d++) S.bias[d] = col[d];
         } else {
           rnea(m, S.qb, zeros, vec, S.ct, S.st, 0.0, S.fex, S.fez, S.tex, false, col);
-          for (int i = 0; i < nd; i++) S.M[i * kMaxD + lane] = col[i];
+          for (int i = 0; i < nd; i++) S.M[i * kMaxD + it] = col[i];
         }
       }
       __syncwarp();
-      if (lane < nd) S.rhs[lane] = S.tau[lane] - S.bias[lane];
+      for (int d = lane; d < nd; d += kLanes) S.rhs[d] = S.tau[d] - S.bias[d];
       // Cholesky (physics.py:241-269 / solve_spd): column j, then its rows
       for (int j = active0; j < nd; j++) {
         if (lane == 0) {
@@ -454,8 +456,7 @@ __global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(Step
           S.M[j * kMaxD + j] = sqrt(acc);
         }
         __syncwarp();
-        const int i = lane;
-        if (i > j && i < nd) {
+        for (int i = j + 1 + lane; i < nd; i += kLanes) {
           double acc = S.M[i * kMaxD + j];
           for (int t = active0; t < j; t++) acc -= S.M[i * kMaxD + t] * S.M[j * kMaxD + t];
           S.M[i * kMaxD + j] = acc / S.M[j * kMaxD + j];
@@ -477,8 +478,7 @@ __global__ void __launch_bounds__(kPhysWarps * 32) physics_step_warp_kernel(Step
         }
       }
       __syncwarp();
-      if (lane < nd) {  // semi-implicit Euler (physics.py:389-398)
-        const int d = lane;
+      for (int d = lane; d < nd; d += kLanes) {  // semi-implicit Euler (physics.py:389-398)
         double v = S.qdb[d] + a.h * S.qdd[d];
         if (v > VEL_CLAMP) v = VEL_CLAMP;
         else if (v < -VEL_CLAMP) v = -VEL_CLAMP;
@@ -634,13 +634,12 @@ __global__ void fk_env_kernel(const double *qpos, const int32_t *parent, const d
   }
 }
 
-// measured crossover (tools/phys_bench.py, B200): warp-per-env is 1.6-2.4x
-// faster up to ~1-2k envs, one thread per env wins from ~4k on
-constexpr int64_t kWarpEnvMax = 2048;
-// half a warp per env (nd < 16) beats a whole warp at every batch and one
-// thread per env up to ~4k envs for the larger models (Humanoid 0.61 vs
-// 0.76 ms at 4096), ~2-3k for the smaller ones
-constexpr int64_t kHalfEnvMaxLarge = 4096, kHalfEnvMaxSmall = 2048;
+// Lanes per env by batch (tools/phys_bench.py on a B200, Humanoid / HalfCheetah):
+// one warp per env is fastest up to ~1k envs (B=1: 0.17 / 0.10 ms against
+// 0.65 / 0.25 ms for one thread per env), half a warp up to 2k, a quarter
+// warp up to ~6k for models of 10+ dofs (B=4096: 0.57 against 0.76 ms), one
+// thread per env above (B=16384: 1.05 against 1.76 ms for a quarter warp).
+constexpr int64_t kWarpEnvMax = 1024, kHalfEnvMax = 2048, kQuarterEnvMax = 6144;
 
 static inline unsigned blocks_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
@@ -682,23 +681,26 @@ extern "C" pxr_status pxr_physics_step(const pxr_model *model, double *qpos, dou
   a.forward_weight = model->forward_weight;
   a.ctrl_cost = model->ctrl_cost;
   a.ep_len = model->episode_length;
-  // half a warp per env (nd < 16) or a whole warp (larger models) in the
-  // latency-bound range, one thread per env above
-  // (throughput); PXR_DEBUG_PHYS=warp|half|thread forces one
+  // sub-warp kernels in the latency-bound range, one thread per env above
+  // (throughput); PXR_DEBUG_PHYS=warp|half|quarter|thread forces one
   const char *force = getenv("PXR_DEBUG_PHYS");
   const int nd = model->n_links + 2;
-  const int64_t half_max = nd >= 12 ? kHalfEnvMaxLarge : kHalfEnvMaxSmall;
-  char kind = nd < 16 && batch <= half_max ? 'h' : (batch <= kWarpEnvMax ? 'w' : 't');
+  char kind = batch <= kWarpEnvMax                  ? 'w'
+              : batch <= kHalfEnvMax                  ? 'h'
+              : (nd >= 12 && batch <= kQuarterEnvMax) ? 'q'
+                                                      : 't';
   if (force != nullptr) kind = force[0];
-  if (kind == 'h' && nd >= 16) kind = 'w';
-  if (kind == 'w') {
-    physics_step_warp_kernel<32><<<blocks_for((batch + kPhysWarps - 1) / kPhysWarps, 1),
-                                   kPhysWarps * 32, 0, (cudaStream_t)stream>>>(a);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kind == 'w') {  // 4 envs per 128-thread block
+    physics_step_warp_kernel<32><<<blocks_for((batch + 3) / 4, 1), 128, 0, st>>>(a);
     return check_launch("physics_step_warp_kernel");
   }
-  if (kind == 'h') {
-    physics_step_warp_kernel<16><<<blocks_for((batch + 2 * kPhysWarps - 1) / (2 * kPhysWarps), 1),
-                                   kPhysWarps * 32, 0, (cudaStream_t)stream>>>(a);
+  if (kind == 'h') {  // 8 envs per 128-thread block
+    physics_step_warp_kernel<16><<<blocks_for((batch + 7) / 8, 1), 128, 0, st>>>(a);
+    return check_launch("physics_step_warp_kernel");
+  }
+  if (kind == 'q') {  // 8 envs per 64-thread block
+    physics_step_warp_kernel<8><<<blocks_for((batch + 7) / 8, 1), 64, 0, st>>>(a);
     return check_launch("physics_step_warp_kernel");
   }
   physics_step_kernel<<<blocks_for(batch, 64), 64, 0, (cudaStream_t)stream>>>(a);

@@ -80,7 +80,7 @@ class TestPhysicsAPI:
         rng = np.random.default_rng(11)
         acts = rng.uniform(-1.5, 1.5, (60,) + rec[f"{name}_act"].shape)
         finals = []
-        for kind in ("warp", "thread", "half"):
+        for kind in ("warp", "thread", "half", "quarter"):
             monkeypatch.setenv("PXR_DEBUG_PHYS", kind)
             st = pkg.SystemState(torch.from_numpy(rec[f"{name}_qpos"]).cuda(),
                                  torch.from_numpy(rec[f"{name}_qvel"]).cuda(),

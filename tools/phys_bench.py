@@ -12,7 +12,7 @@ for model in ("humanoid_lite", "cheetah_lite"):
         env, s, obs = E.make_env(E.EnvConfig(model=STANDIN_MODELS.get(model, model), batch=B))
         act = torch.zeros((B, env.n_joints), dtype=torch.float64, device='cuda')
         res = []
-        for kind in ("thread", "warp", "half"):
+        for kind in ("thread", "warp", "half", "quarter"):
             os.environ["PXR_DEBUG_PHYS"] = kind
             sysc = s.sys.copy(); rew = torch.zeros(B, dtype=torch.float64, device='cuda')
             f = lambda: L.pxr_physics_step(ctypes.byref(env.model_c), sysc.qpos.data_ptr(), sysc.qvel.data_ptr(), sysc.step_count.data_ptr(), sysc.done.data_ptr(), act.data_ptr(), rew.data_ptr(), B, _native.stream_ptr())
@@ -22,5 +22,5 @@ for model in ("humanoid_lite", "cheetah_lite"):
             torch.cuda.synchronize(); a.record()
             for _ in range(n): f()
             b.record(); torch.cuda.synchronize(); res.append(a.elapsed_time(b) / n)
-        print(f"{model} B={B}: thread {res[0]:.3f} ms  warp {res[1]:.3f} ms  half {res[2]:.3f} ms", flush=True)
+        print(f"{model} B={B}: thread {res[0]:.3f} ms  warp {res[1]:.3f} ms  half {res[2]:.3f} ms  quarter {res[3]:.3f} ms", flush=True)
         del env, s, obs
