@@ -302,6 +302,9 @@ conv_proj_kernel(const float *__restrict__ feat, int64_t batch, int K,
       }
       __syncthreads();
       if (env < batch) {
+        // (unrolled: several feature loads in flight; each output's FMA
+        // chain keeps its order)
+#pragma unroll 4
         for (int kk = lane; kk < kn; kk += 32) {
           const float v = __ldg(fr + k0 + kk);
           const float4 *pr = reinterpret_cast<const float4 *>(s_p + kk * JP);
