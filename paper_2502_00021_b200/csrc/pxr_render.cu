@@ -485,21 +485,6 @@ __device__ __forceinline__ void put_rgb(uint8_t *col, uint32_t pix, uint32_t rgb
   col[3 * pix + 2] = (uint8_t)(rgb >> 16);
 }
 
-// Insert 24-bit texel t as pixel k (0..3) of a 12-byte, 3-word RGB group.
-__device__ __forceinline__ void put_texel(uint32_t w[3], int k, uint32_t t) {
-  if (k == 0) {
-    w[0] = (w[0] & 0xff000000u) | t;
-  } else if (k == 1) {
-    w[0] = (w[0] & 0x00ffffffu) | (t << 24);
-    w[1] = (w[1] & 0xffff0000u) | (t >> 8);
-  } else if (k == 2) {
-    w[1] = (w[1] & 0x0000ffffu) | (t << 16);
-    w[2] = (w[2] & 0xffffff00u) | (t >> 16);
-  } else {
-    w[2] = (w[2] & 0x000000ffu) | (t << 8);
-  }
-}
-
 // kBands = false: the whole frame is one band (y0 = 0, straight-line code).
 // kFloor = draw_floor: the checker floor needs every thread for the
 // background (f64 per pixel), without it the background is cheap enough for
