@@ -270,7 +270,7 @@ conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
 }
 
-constexpr int kProjEnvs = 8;
+constexpr int kProjEnvs = 16;
 constexpr int kProjTile = 256;  // proj rows per shared-memory tile
 
 // JP = J rounded up to a multiple of 4: the staged proj rows are padded with
