@@ -88,6 +88,12 @@ def test_validation_without_gpu(native):
     assert st == native.PXR_ERR_INVALID
     assert lib.pxr_apply_color(None, None, 1, 8, 8, None) == native.PXR_ERR_INVALID
     assert lib.pxr_grayscale(None, None, 4, None) == native.PXR_ERR_INVALID
+    # ABI v2: the standalone distractor advance takes host keys only
+    d = native.Distractor(native.MODE_COLOR)
+    keys = native.StepKeys(1, 2, 0, 4, 12345)
+    st = lib.pxr_advance_distractors(ctypes.byref(d), None, 4, ctypes.byref(keys), None, None)
+    assert st == native.PXR_ERR_UNSUPPORTED and b"device_key" in lib.pxr_last_error()
+    assert lib.pxr_step_key_advance(0, 0, None, None, None) == native.PXR_ERR_INVALID
 
 
 def test_product_never_imports_oracle():
