@@ -5,6 +5,8 @@ poses, and a video pack of odd size (so both the byte-permute gather and the
 generic texel path run). Pixels, depth and the distractor composite must be
 bit-exact for every case."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -28,7 +30,8 @@ def _case(seed):
     return rng, name, mode, H, W, band, offset, fov, fib, gray, hv, wv
 
 
-@pytest.mark.parametrize("seed", range(40))
+# PXR_FUZZ_SEEDS=N widens the sweep for soak runs (default 40)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("PXR_FUZZ_SEEDS", "40"))))
 def test_fused_render_fuzz_vs_oracle(pkg, torch, oracle, monkeypatch, seed):
     rng, name, mode, H, W, band, offset, fov, fib, gray, hv, wv = _case(seed)
     if band:
