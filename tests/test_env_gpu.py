@@ -229,7 +229,9 @@ class TestStepGraph:
             path = tmp_path / "p.pxvp"
             save_video_pack(synthetic_pack(), path)
             kw["video_pack_path"] = str(path)
-        B, T = 24, 120  # long enough for walker falls: resets + video re-draws
+        # long enough for walker falls: resets + video re-draws (PXR_SOAK_STEPS
+        # lengthens it for soak runs)
+        B, T = 24, int(os.environ.get("PXR_SOAK_STEPS", "120"))
         env, s0, obs0 = _env(E, name, batch=B, seed=3, distractor_mode=mode, **kw)
         stub = ConvStub.create(84, 84, int(obs0.shape[-1]), env.n_joints, seed=0)
         # reference: the pure step loop
