@@ -20,14 +20,16 @@
 //   2. triangle liveness exactly as the reference culls (near/far, zero
 //      area, empty pixel bbox); a block scan over the triangles in index
 //      order gives live index + bbox-row prefix; the background (sky, floor,
-//      video texel) under an empty z-buffer, written as final colours;
+//      video texel) under an empty z-buffer, written as final colours (with
+//      the floor here, without it by the warps phase 3 leaves idle);
 //   3. per round of live triangles (one round whenever the records fit): a
 //      record per triangle (edge vectors, exact reciprocal of the area, flat
 //      colour, the degenerate-normal cull) plus f32 line equations for
 //      conservative row spans; (triangle, bbox row) units in 32-row chunks
 //      dealt to the warps: each lane computes one row's conservative span,
 //      non-empty spans gather in a per-warp queue and every 32 are expanded
-//      into pixel candidates (warp scan + owner search) for the reference's
+//      into pixel candidates (warp scan + owner search), whole rounds of 32
+//      candidates at a time (the rest re-queued), for the reference's
 //      exact f64 edge / barycentric / depth arithmetic; covered fragments
 //      min-reduce their f32 depth per pixel with a 32-bit shared-memory
 //      atomicMin and are appended to a fragment list;
