@@ -229,7 +229,8 @@ pxr_status pxr_reset_envs(const pxr_model *model, double *qpos, double *qvel,
 pxr_status pxr_step_key_advance(uint64_t master_hi, uint64_t master_lo, int64_t *t,
                                 uint64_t *key_out, void *stream);
 
-/* forward_kinematics for an env's model: qpos (B, L + 2) -> poses (B, L, 3). */
+/* forward_kinematics (physics.py:114-137, Env._render_frame env.py:155-166)
+ * for an env's model: qpos (B, L + 2) -> poses (B, L, 3). */
 pxr_status pxr_env_poses(const pxr_model *model, const double *qpos, int64_t batch,
                          double *poses, void *stream);
 
