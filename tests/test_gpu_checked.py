@@ -24,7 +24,9 @@ pytestmark = pytest.mark.gpu
 CHECKED = os.path.join(REPO, "paper_2502_00021_b200", "libpxr_checked.so")
 SUITES = ["tests/test_gpu_fuzz.py", "tests/test_gpu_parity.py", "tests/test_policy.py",
           "tests/test_physics_api.py", "tests/test_env_gpu.py", "tests/test_scenes.py",
-          "tests/test_gpu_determinism.py"]
+          "tests/test_gpu_determinism.py", "tests/test_gpu_render_api.py",
+          "tests/test_gpu_distractor_api.py", "tests/test_gpu_env_api.py",
+          "tests/test_gpu_physics_props.py", "tests/test_recorder_api.py"]
 
 
 def test_parity_suites_under_device_checks():
