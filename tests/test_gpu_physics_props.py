@@ -36,6 +36,7 @@ def free_link(M, dt=1e-3, substeps=5):
 
 
 def state_from_qpos(P, torch, qpos, qvel=None):
+    """A SystemState on the device from host generalized coordinates."""
     q = np.atleast_2d(np.asarray(qpos, dtype=np.float64))
     v = np.zeros_like(q) if qvel is None else np.atleast_2d(np.asarray(qvel, dtype=np.float64))
     b = q.shape[0]
@@ -60,136 +61,121 @@ def test_resting_link_is_stationary(P, M, torch):
     assert np.max(np.abs(host(s.qpos) - before)) < 1e-6
 
 
-class TestRewardAndTermination:
-    def test_reward_terms(self, P, M, torch):
-        spec = M.builtin_model("cheetah_lite")
-        s = state_from_qpos(P, torch, np.tile(spec.rest(), (1, 1)))
-        assert float(P.compute_reward(spec, s, s, np.zeros((1, spec.n_joints)))[0]) == 0.0
-        fl = dataclasses.replace(free_link(M), dt=0.05, forward_weight=1.0)
-        a = state_from_qpos(P, torch, [0.0, 1.0, 0.0])
-        b = state_from_qpos(P, torch, [0.1, 1.0, 0.0])
-        assert float(P.compute_reward(fl, a, b, np.zeros((1, 0)))[0]) == pytest.approx(2.0)
-        acts = np.array([[1.0, -1.0, 1.0, -1.0, 1.0, -1.0]])  # ctrl_cost 0.1, six joints
-        assert float(P.compute_reward(spec, s, s, acts)[0]) == pytest.approx(-0.6)
-        assert np.array_equal(host(P.compute_reward(spec, s, s, np.full((1, 6), 50.0))),
-                              host(P.compute_reward(spec, s, s, np.ones((1, 6)))))
-
-    def test_termination(self, P, M, torch):
-        c = M.builtin_model("cheetah_lite")
-        q = np.tile(c.rest(), (3, 1))
-        q[:, 1] = [-5.0, 0.0, 5.0]
-        assert not host(P.check_termination(c, state_from_qpos(P, torch, q))).any()
-        w = M.builtin_model("walker_lite")
-        q = np.tile(w.rest(), (1, 1))
-        q[0, 1] = 0.5
-        assert host(P.check_termination(w, state_from_qpos(P, torch, q)))[0]
-        q[0, 1] = 0.8  # the boundary is strict
-        assert not host(P.check_termination(w, state_from_qpos(P, torch, q)))[0]
-
-
-class TestReset:
-    def test_purity_difference_bounds(self, P, M, pkg):
-        w = M.builtin_model("walker_lite")
-        a, b = P.reset_state(w, pkg.key_from_seed(0), 4), P.reset_state(w, pkg.key_from_seed(0), 4)
-        assert np.array_equal(host(a.qpos), host(b.qpos))
-        assert np.array_equal(host(a.qvel), host(b.qvel))
-        s = P.reset_state(w, pkg.key_from_seed(1), 2)
-        assert not np.array_equal(host(s.qpos)[0], host(s.qpos)[1])
-        h = M.builtin_model("hopper_lite")
-        s = P.reset_state(h, pkg.key_from_seed(2), 64)
-        assert np.max(np.abs(host(s.qpos) - h.rest())) <= 0.1
-        assert not host(s.done).any() and np.all(host(s.step_count) == 0)
-
-    def test_offset_slice_and_zero_batch(self, P, M, pkg):
-        c = M.builtin_model("cheetah_lite")
-        k = pkg.key_from_seed(3)
-        big, tail = P.reset_state(c, k, 10), P.reset_state(c, k, 3, env_offset=7)
-        assert np.array_equal(host(big.qpos)[7:], host(tail.qpos))
-        assert np.array_equal(host(big.qvel)[7:], host(tail.qvel))
-        with pytest.raises(ValueError):
-            P.reset_state(c, k, 0)
+def test_reward_terms_and_termination(P, M, torch):
+    ch = M.builtin_model("cheetah_lite")
+    rest = state_from_qpos(P, torch, ch.rest()[None])
+    reward = lambda spec, a, b, u: host(P.compute_reward(spec, a, b, u))  # noqa: E731
+    # (spec, prev, next, actions) -> expected reward
+    glide = dataclasses.replace(free_link(M), dt=0.05, forward_weight=1.0)
+    table = [
+        (ch, rest, rest, np.zeros((1, 6)), 0.0),
+        (glide, state_from_qpos(P, torch, [0.0, 1.0, 0.0]),
+         state_from_qpos(P, torch, [0.1, 1.0, 0.0]), np.zeros((1, 0)), 2.0),  # 0.1 / 0.05
+        (ch, rest, rest, np.array([[1.0, -1.0] * 3]), -0.6),  # ctrl cost 0.1 x six joints
+    ]
+    for spec, a, b, u, want in table:
+        assert float(reward(spec, a, b, u)[0]) == pytest.approx(want)
+    assert np.array_equal(reward(ch, rest, rest, np.full((1, 6), 50.0)),
+                          reward(ch, rest, rest, np.ones((1, 6))))  # actions clamp to [-1, 1]
+    heights = np.tile(ch.rest(), (3, 1))
+    heights[:, 1] = (-5.0, 0.0, 5.0)  # the cheetah never terminates
+    assert not host(P.check_termination(ch, state_from_qpos(P, torch, heights))).any()
+    wk = M.builtin_model("walker_lite")
+    for z, terminated in ((0.5, True), (0.8, False)):  # below 0.8 only (strict)
+        q = wk.rest()[None].copy()
+        q[0, 1] = z
+        assert bool(host(P.check_termination(wk, state_from_qpos(P, torch, q)))[0]) is terminated
 
 
-class TestBatchSemantics:
-    @staticmethod
-    def _acts(pkg, spec, seed, t, ids):
-        from paper_2502_00021_b200.prng import fold_in, uniform
-
-        k = pkg.key_from_seed(seed)
-        return np.stack([uniform(fold_in(fold_in(k, t), i), spec.n_joints, -1.0, 1.0)
-                         for i in ids])
-
-    def test_purity_and_order_equivariance(self, P, M, pkg, torch):
-        h = M.builtin_model("hopper_lite")
-        s0 = P.reset_state(h, pkg.key_from_seed(4), 3)
-        acts = np.full((3, h.n_joints), 0.3)
-        a, b = P.step_dynamics(h, s0, acts), P.step_dynamics(h, s0, acts)
-        assert np.array_equal(host(a.qpos), host(b.qpos))
-        w = M.builtin_model("walker_lite")
-        s0 = P.reset_state(w, pkg.key_from_seed(5), 8)
-        rng = np.random.default_rng(0)
-        acts = rng.uniform(-1, 1, (8, w.n_joints))
-        perm = rng.permutation(8)
-        out = P.step_dynamics(w, s0, acts)
-        pi = torch.from_numpy(perm).cuda()
-        sp = P.SystemState(s0.qpos[pi], s0.qvel[pi], s0.step_count[pi], s0.done[pi])
-        outp = P.step_dynamics(w, sp, acts[perm])
-        assert np.array_equal(host(outp.qpos), host(out.qpos)[perm])
-        assert np.array_equal(host(outp.qvel), host(out.qvel)[perm])
-
-    def test_batch_size_independence(self, P, M, pkg):
-        c = M.builtin_model("cheetah_lite")
-        big = P.reset_state(c, pkg.key_from_seed(6), 16)
-        i = 11
-        one = P.SystemState(big.qpos[i:i + 1].clone(), big.qvel[i:i + 1].clone(),
-                            big.step_count[i:i + 1].clone(), big.done[i:i + 1].clone())
-        for t in range(50):
-            big = P.step_dynamics(c, big, self._acts(pkg, c, 7, t, range(16)))
-            one = P.step_dynamics(c, one, self._acts(pkg, c, 7, t, [i]))
-        assert np.array_equal(host(one.qpos)[0], host(big.qpos)[i])
-        assert np.array_equal(host(one.qvel)[0], host(big.qvel)[i])
-
-    def test_clamp_shape_and_episode_length(self, P, M, pkg, torch):
-        h = M.builtin_model("hopper_lite")
-        s0 = P.reset_state(h, pkg.key_from_seed(10), 2)
-        a = P.step_dynamics(h, s0, np.full((2, h.n_joints), 10.0))
-        b = P.step_dynamics(h, s0, np.ones((2, h.n_joints)))
-        assert np.array_equal(host(a.qpos), host(b.qpos))
-        with pytest.raises(ValueError):
-            P.step_dynamics(h, s0, np.zeros((2, h.n_joints + 1)))
-        spec = dataclasses.replace(free_link(M), episode_length=3)
-        s = state_from_qpos(P, torch, [0.0, 5.0, 0.0])
-        for _ in range(3):
-            assert not bool(s.done[0])
-            s = P.step_dynamics(spec, s, np.zeros((1, 0)))
-        assert bool(s.done[0]) and int(s.step_count[0]) == 3
+def test_reset_draws(P, M, pkg):
+    seed = pkg.key_from_seed
+    walker, hopper, cheetah = (M.builtin_model(n) for n in ("walker_lite", "hopper_lite",
+                                                             "cheetah_lite"))
+    first, again = (P.reset_state(walker, seed(0), 4) for _ in range(2))
+    for field in ("qpos", "qvel"):
+        assert np.array_equal(host(getattr(first, field)), host(getattr(again, field)))
+    pair = host(P.reset_state(walker, seed(1), 2).qpos)
+    assert not np.array_equal(pair[0], pair[1])
+    many = P.reset_state(hopper, seed(2), 64)
+    assert np.abs(host(many.qpos) - hopper.rest()).max() <= 0.1  # U(-0.1, 0.1) around rest
+    assert not host(many.done).any() and not host(many.step_count).any()
+    whole, last3 = P.reset_state(cheetah, seed(3), 10), P.reset_state(cheetah, seed(3), 3,
+                                                                      env_offset=7)
+    for field in ("qpos", "qvel"):  # env_offset reproduces the batch slice
+        assert np.array_equal(host(getattr(whole, field))[7:], host(getattr(last3, field)))
+    with pytest.raises(ValueError):
+        P.reset_state(cheetah, seed(3), 0)
 
 
-class TestForwardKinematics:
-    def test_root_and_translation(self, P, M):
-        c = M.builtin_model("cheetah_lite")
-        q = np.tile(c.rest(), (1, 1))
-        assert np.array_equal(np.asarray(P.forward_kinematics(c, q).cpu())[0, 0], q[0, :3])
-        w = M.builtin_model("walker_lite")
-        q = np.tile(w.rest(), (1, 1))
-        base = P.forward_kinematics(w, q).cpu().numpy()
-        q2 = q.copy()
-        q2[0, 0] += 3.0
-        q2[0, 1] -= 0.5
-        moved = P.forward_kinematics(w, q2).cpu().numpy()
-        assert np.allclose(moved[0, :, 0], base[0, :, 0] + 3.0)
-        assert np.allclose(moved[0, :, 1], base[0, :, 1] - 0.5)
-        assert np.array_equal(moved[0, :, 2], base[0, :, 2])
+def _policy_actions(pkg, spec, seed, t, env_ids):
+    from paper_2502_00021_b200.prng import fold_in, uniform
 
-    def test_hand_oracles_and_shape(self, P, M):
-        elbow = M.ModelSpec("elbow", (M.LinkSpec(2.0, 1.0, 0.05), M.LinkSpec(1.0, 1.0, 0.05)),
-                            (M.JointSpec(0, -3.0, 3.0, 1.0, anchor=1.0),))
-        p = P.forward_kinematics(elbow, np.array([[0.0, 0.0, 0.0, np.pi / 2]])).cpu().numpy()
-        assert np.allclose(p[0, 1], [2.0, 0.0, np.pi / 2])
-        mid = M.ModelSpec("mid", (M.LinkSpec(2.0, 1.0, 0.05), M.LinkSpec(1.0, 1.0, 0.05)),
-                          (M.JointSpec(0, -3.0, 3.0, 1.0, anchor=0.5),))
-        p = P.forward_kinematics(mid, np.array([[0.0, 0.0, np.pi / 2, 0.0]])).cpu().numpy()
-        assert np.allclose(p[0, 1], [0.0, 1.0, np.pi / 2])
-        h = M.builtin_model("hopper_lite")
-        with pytest.raises(ValueError):
-            P.forward_kinematics(h, np.zeros((1, h.dof + 2)))
+    step_key = fold_in(pkg.key_from_seed(seed), t)
+    return np.stack([uniform(fold_in(step_key, e), spec.n_joints, -1.0, 1.0) for e in env_ids])
+
+
+def test_batch_semantics(P, M, pkg, torch):
+    hop = M.builtin_model("hopper_lite")
+    s0 = P.reset_state(hop, pkg.key_from_seed(4), 3)
+    u = np.full((3, hop.n_joints), 0.3)
+    assert np.array_equal(host(P.step_dynamics(hop, s0, u).qpos),
+                          host(P.step_dynamics(hop, s0, u).qpos))  # pure
+    wk = M.builtin_model("walker_lite")
+    s8 = P.reset_state(wk, pkg.key_from_seed(5), 8)
+    g = np.random.default_rng(0)
+    u8 = g.uniform(-1, 1, (8, wk.n_joints))
+    order = g.permutation(8)
+    idx = torch.from_numpy(order).cuda()
+    shuffled = P.SystemState(*(getattr(s8, f)[idx] for f in ("qpos", "qvel", "step_count",
+                                                            "done")))
+    ref, perm = P.step_dynamics(wk, s8, u8), P.step_dynamics(wk, shuffled, u8[order])
+    for field in ("qpos", "qvel"):  # permuting the batch permutes the results
+        assert np.array_equal(host(getattr(perm, field)), host(getattr(ref, field))[order])
+    ch = M.builtin_model("cheetah_lite")
+    batch16 = P.reset_state(ch, pkg.key_from_seed(6), 16)
+    k = 11
+    solo = P.SystemState(*(getattr(batch16, f)[k:k + 1].clone()
+                           for f in ("qpos", "qvel", "step_count", "done")))
+    for t in range(50):  # env k alone steps exactly like env k of 16
+        batch16 = P.step_dynamics(ch, batch16, _policy_actions(pkg, ch, 7, t, range(16)))
+        solo = P.step_dynamics(ch, solo, _policy_actions(pkg, ch, 7, t, [k]))
+    for field in ("qpos", "qvel"):
+        assert np.array_equal(host(getattr(solo, field))[0], host(getattr(batch16, field))[k])
+
+
+def test_action_limits_shapes_and_episode_length(P, M, pkg, torch):
+    hop = M.builtin_model("hopper_lite")
+    s0 = P.reset_state(hop, pkg.key_from_seed(10), 2)
+    ten, one = (P.step_dynamics(hop, s0, np.full((2, hop.n_joints), v)) for v in (10.0, 1.0))
+    assert np.array_equal(host(ten.qpos), host(one.qpos))
+    with pytest.raises(ValueError):
+        P.step_dynamics(hop, s0, np.zeros((2, hop.n_joints + 1)))
+    short = dataclasses.replace(free_link(M), episode_length=3)
+    s = state_from_qpos(P, torch, [0.0, 5.0, 0.0])
+    flags = []
+    for _ in range(3):
+        flags.append(bool(s.done[0]))
+        s = P.step_dynamics(short, s, np.zeros((1, 0)))
+    assert flags == [False] * 3 and bool(s.done[0]) and int(s.step_count[0]) == 3
+
+
+def test_forward_kinematics(P, M):
+    fk = lambda spec, q: P.forward_kinematics(spec, np.asarray(q, float)).cpu().numpy()  # noqa
+    ch = M.builtin_model("cheetah_lite")
+    assert np.array_equal(fk(ch, ch.rest()[None])[0, 0], ch.rest()[:3])  # root passes through
+    wk = M.builtin_model("walker_lite")
+    q = wk.rest()[None].copy()
+    moved = q.copy()
+    moved[0, :2] += (3.0, -0.5)
+    a, b = fk(wk, q), fk(wk, moved)
+    assert np.allclose(b[0, :, :2], a[0, :, :2] + (3.0, -0.5))
+    assert np.array_equal(b[0, :, 2], a[0, :, 2])
+    two_links = (M.LinkSpec(2.0, 1.0, 0.05), M.LinkSpec(1.0, 1.0, 0.05))
+    # (anchor along the parent, qpos, expected child pose) worked by hand
+    for anchor, qpos, child in ((1.0, (0.0, 0.0, 0.0, np.pi / 2), (2.0, 0.0, np.pi / 2)),
+                                (0.5, (0.0, 0.0, np.pi / 2, 0.0), (0.0, 1.0, np.pi / 2))):
+        spec = M.ModelSpec("hand", two_links, (M.JointSpec(0, -3.0, 3.0, 1.0, anchor=anchor),))
+        assert np.allclose(fk(spec, [qpos])[0, 1], child)
+    hop = M.builtin_model("hopper_lite")
+    with pytest.raises(ValueError):
+        fk(hop, np.zeros((1, hop.dof + 2)))
