@@ -38,17 +38,31 @@ STRIDE = 4
 N_FILTERS = 16
 
 
+def _glorot(key, rows: int, cols: int) -> np.ndarray:
+    """(rows, cols) float32 Glorot-uniform weights from one Threefry stream
+    (the reference's draw: uniform(key, rows * cols, -s, s), s = sqrt(6 / rows))."""
+    s = float(np.sqrt(6.0 / rows))
+    return uniform(key, rows * cols, -s, s).astype(np.float32).reshape(rows, cols)
+
+
+def _quadrant_blocks(conv: np.ndarray, channels: int) -> np.ndarray:
+    """The 8x8 kernel as its four 4x4 quadrants side by side: column block q
+    = 2 dy + dx holds quadrant (dy, dx) (the reference's conv_blocks)."""
+    k = conv.reshape(2, STRIDE, 2, STRIDE, channels, N_FILTERS)
+    quads = [k[q // 2, :, q % 2].reshape(-1, N_FILTERS) for q in range(4)]
+    return np.ascontiguousarray(np.hstack(quads), dtype=np.float32)
+
+
 @dataclass(frozen=True)
 class ConvStub:
-    """Fixed policy surrogate; weights are a pure function of the seed
-    (bench.py:40-88): Glorot-uniform Threefry draws ``uniform(fold_in(key,
-    0))`` for the conv (row order (ky, kx, c)) and ``uniform(fold_in(key, 1))``
-    for the projection (feature order (oy, ox, f)), cast to float32.
-    ``conv_blocks`` (the reference's quadrant layout) is kept for API parity."""
+    """The reference's fixed policy surrogate (bench.py:40-88); weights are a
+    pure function of the seed: conv rows in (ky, kx, c) order from stream
+    fold_in(key, 0), projection rows in (oy, ox, f) order from fold_in(key, 1).
+    ``conv_blocks`` keeps the reference's quadrant layout for API parity."""
 
-    conv: np.ndarray  # (K*K*C, filters) float32
+    conv: np.ndarray         # (K*K*C, filters) float32
     conv_blocks: np.ndarray  # (STRIDE*STRIDE*C, 4*filters) float32
-    proj: np.ndarray  # (out_h*out_w*filters, n_joints) float32
+    proj: np.ndarray         # (out_h*out_w*filters, n_joints) float32
     height: int
     width: int
     channels: int
@@ -56,26 +70,14 @@ class ConvStub:
 
     @classmethod
     def create(cls, height: int, width: int, channels: int, n_joints: int, seed: int = 0):
-        out_h = (height - KERNEL_SIZE) // STRIDE + 1
-        out_w = (width - KERNEL_SIZE) // STRIDE + 1
-        if out_h < 1 or out_w < 1:
+        positions = ((height - KERNEL_SIZE) // STRIDE + 1) * ((width - KERNEL_SIZE) // STRIDE + 1)
+        if height < KERNEL_SIZE or width < KERNEL_SIZE:
             raise ValueError("observation smaller than the conv kernel")
-        key = key_from_seed(seed)
-        fan_in = KERNEL_SIZE * KERNEL_SIZE * channels
-        lim = np.sqrt(6.0 / fan_in)
-        conv = uniform(fold_in(key, 0), fan_in * N_FILTERS, -lim, lim)
-        conv = conv.astype(np.float32).reshape(fan_in, N_FILTERS)
-        feat = out_h * out_w * N_FILTERS
-        plim = np.sqrt(6.0 / feat)
-        proj = uniform(fold_in(key, 1), feat * n_joints, -plim, plim)
-        # quadrant q = 2*dy + dx of the 8x8 kernel -> columns [16q, 16q + 16)
-        k = conv.reshape(2, STRIDE, 2, STRIDE, channels, N_FILTERS)
-        blocks = np.concatenate(
-            [k[dy, :, dx].reshape(STRIDE * STRIDE * channels, N_FILTERS)
-             for dy in range(2) for dx in range(2)], axis=1).astype(np.float32)
-        return cls(conv=conv, conv_blocks=np.ascontiguousarray(blocks),
-                   proj=proj.astype(np.float32).reshape(feat, n_joints), height=height,
-                   width=width, channels=channels, n_joints=n_joints)
+        root = key_from_seed(seed)
+        conv = _glorot(fold_in(root, 0), KERNEL_SIZE * KERNEL_SIZE * channels, N_FILTERS)
+        proj = _glorot(fold_in(root, 1), positions * N_FILTERS, n_joints)
+        return cls(conv, _quadrant_blocks(conv, channels), proj, height, width, channels,
+                   n_joints)
 
     def device_weights(self, device):
         """(conv, proj) float32 CUDA tensors, uploaded once per device."""
@@ -197,30 +199,38 @@ def run_benchmark(config: BenchConfig, progress=None) -> list:
 
 # ---------------------------------------------------------------- CSV
 
-_CSV_HEADER = "env,batch,distractor,steps,seconds,sps,resolution"
+_CSV_COLUMNS = ("env", "batch", "distractor", "steps", "seconds", "sps", "resolution")
+_CSV_HEADER = ",".join(_CSV_COLUMNS)
+
+
+def _csv_row(r: BenchRecord) -> str:
+    """One record in the reference's CSV schema (bench.py:239-250): floats
+    at 6 significant digits, the digest left out."""
+    cells = (r.env_name, r.batch, r.distractor_mode, r.steps_measured,
+             f"{r.wall_seconds:.6g}", f"{r.steps_per_second:.6g}", r.resolution)
+    return ",".join(str(c) for c in cells)
 
 
 def write_csv(records, path) -> None:
-    """bench.py:239-250: floats at 6 significant digits."""
     try:
-        with open(path, "w") as f:
-            f.write(_CSV_HEADER + "\n")
-            for r in records:
-                f.write(f"{r.env_name},{r.batch},{r.distractor_mode},{r.steps_measured},"
-                        f"{r.wall_seconds:.6g},{r.steps_per_second:.6g},{r.resolution}\n")
+        with open(path, "w") as fh:
+            fh.write("\n".join([_CSV_HEADER] + [_csv_row(r) for r in records]) + "\n")
     except OSError as e:
         raise OSError(f"cannot write benchmark CSV to {path}: {e}") from e
 
 
 def read_csv(path) -> list:
-    with open(path) as f:
-        lines = [ln.rstrip("\n") for ln in f if ln.strip()]
-    if not lines or lines[0] != _CSV_HEADER:
+    with open(path) as fh:
+        rows = [line.strip() for line in fh if line.strip()]
+    if not rows or rows[0] != _CSV_HEADER:
         raise ValueError(f"{path}: missing benchmark CSV header")
     out = []
-    for ln in lines[1:]:
-        env_name, batch, mode, steps, seconds, sps, res = ln.split(",")
-        out.append(BenchRecord(env_name=env_name, batch=int(batch), distractor_mode=mode,
-                               steps_measured=int(steps), wall_seconds=float(seconds),
-                               steps_per_second=float(sps), resolution=res))
+    for line in rows[1:]:
+        cell = dict(zip(_CSV_COLUMNS, line.split(",")))
+        out.append(BenchRecord(env_name=cell["env"], batch=int(cell["batch"]),
+                               distractor_mode=cell["distractor"],
+                               steps_measured=int(cell["steps"]),
+                               wall_seconds=float(cell["seconds"]),
+                               steps_per_second=float(cell["sps"]),
+                               resolution=cell["resolution"]))
     return out
