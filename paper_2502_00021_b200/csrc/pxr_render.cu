@@ -65,7 +65,10 @@
 
 namespace pxr {
 
-constexpr int kThreads = 768;
+#ifndef PXR_RENDER_THREADS
+#define PXR_RENDER_THREADS 768
+#endif
+constexpr int kThreads = PXR_RENDER_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLinks = 64;
 constexpr uint32_t kFull = 0xffffffffu;
