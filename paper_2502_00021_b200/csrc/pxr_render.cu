@@ -824,6 +824,43 @@ render_step_kernel(const RenderParams p) {
             reinterpret_cast<float4 *>(s_depth)[gi] = make_float4(inf, inf, inf, inf);
             reinterpret_cast<uint4 *>(s_wkey)[gi] = make_uint4(0u, 0u, 0u, 0u);
           }
+        } else if (kFloor && p.floor_sep && p.mode != PXR_MODE_VIDEO && !p.gray &&
+                   (p.W & 3) == 0) {
+          // separable floor, RGB: 4-pixel groups of one row (W % 4 == 0), the
+          // same per-pixel arithmetic as the scalar loop below, 3 packed
+          // colour words + one float4 depth + one uint4 key store per group
+          const float inf = __int_as_float(0x7f800000);
+          const int n4 = npx >> 2;
+          for (int gi = first; gi < n4; gi += stride) {
+            const int i0 = gi << 2;
+            const int yb = (int)__umulhi((uint32_t)i0, p.wmagic), x = i0 - yb * p.W;
+            const int k = s_fk[y0 + yb];
+            float4 d4 = make_float4(inf, inf, inf, inf);
+            uint32_t c[4] = {kSkyRGB, kSkyRGB, kSkyRGB, kSkyRGB};
+            if (k >= 0) {
+              const double t = s_ft[y0 + yb];
+              const float tf = (float)t;
+              d4 = make_float4(tf, tf, tf, tf);
+              const double2 fa = reinterpret_cast<const double2 *>(s_floor + x)[0];
+              const double2 fb = reinterpret_cast<const double2 *>(s_floor + x)[1];
+              const double fx[4] = {fa.x, fa.y, fb.x, fb.y};
+#pragma unroll
+              for (int j = 0; j < 4; j++) {
+                const double wx = (double)ex + t * fx[j];
+                c[j] = (((uint32_t)__double2ll_rd(wx) ^ (uint32_t)k) & 1u ? 122u : 158u) * 0x010101u;
+              }
+            }
+            if (p.mode == PXR_MODE_COLOR) {
+#pragma unroll
+              for (int j = 0; j < 4; j++) c[j] = __vsubus4(__vaddus4(c[j], bpos), bneg);
+            }
+            uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
+            c3[0] = c[0] | (c[1] << 24);
+            c3[1] = (c[1] >> 8) | (c[2] << 16);
+            c3[2] = (c[2] >> 16) | (c[3] << 8);
+            reinterpret_cast<float4 *>(s_depth)[gi] = d4;
+            reinterpret_cast<uint4 *>(s_wkey)[gi] = make_uint4(0u, 0u, 0u, 0u);
+          }
         } else {
           for (int i = first; i < npx; i += stride) {
             const int yb = (int)__umulhi((uint32_t)i, p.wmagic), x = i - yb * p.W;
