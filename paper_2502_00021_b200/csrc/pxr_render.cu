@@ -824,11 +824,11 @@ render_step_kernel(const RenderParams p) {
             reinterpret_cast<float4 *>(s_depth)[gi] = make_float4(inf, inf, inf, inf);
             reinterpret_cast<uint4 *>(s_wkey)[gi] = make_uint4(0u, 0u, 0u, 0u);
           }
-        } else if (kFloor && p.floor_sep && p.mode != PXR_MODE_VIDEO && !p.gray &&
-                   (p.W & 3) == 0) {
-          // separable floor, RGB: 4-pixel groups of one row (W % 4 == 0), the
-          // same per-pixel arithmetic as the scalar loop below, 3 packed
-          // colour words + one float4 depth + one uint4 key store per group
+        } else if (kFloor && p.floor_sep && p.mode != PXR_MODE_VIDEO && (p.W & 3) == 0) {
+          // separable floor: 4-pixel groups of one row (W % 4 == 0), the same
+          // per-pixel arithmetic as the scalar loop below, 3 packed colour
+          // words (or one word of 4 grey bytes) + one float4 depth + one uint4
+          // key store per group
           const float inf = __int_as_float(0x7f800000);
           const int n4 = npx >> 2;
           for (int gi = first; gi < n4; gi += stride) {
@@ -854,10 +854,19 @@ render_step_kernel(const RenderParams p) {
 #pragma unroll
               for (int j = 0; j < 4; j++) c[j] = __vsubus4(__vaddus4(c[j], bpos), bneg);
             }
-            uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
-            c3[0] = c[0] | (c[1] << 24);
-            c3[1] = (c[1] >> 8) | (c[2] << 16);
-            c3[2] = (c[2] >> 16) | (c[3] << 8);
+            if (p.gray) {  // env.py:168-173, as in emit
+              uint32_t g4 = 0u;
+#pragma unroll
+              for (int j = 0; j < 4; j++)
+                g4 |= ((299u * (c[j] & 0xffu) + 587u * ((c[j] >> 8) & 0xffu) +
+                        114u * ((c[j] >> 16) & 0xffu) + 500u) / 1000u) << (8 * j);
+              reinterpret_cast<uint32_t *>(s_gray)[gi] = g4;
+            } else {
+              uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
+              c3[0] = c[0] | (c[1] << 24);
+              c3[1] = (c[1] >> 8) | (c[2] << 16);
+              c3[2] = (c[2] >> 16) | (c[3] << 8);
+            }
             reinterpret_cast<float4 *>(s_depth)[gi] = d4;
             reinterpret_cast<uint4 *>(s_wkey)[gi] = make_uint4(0u, 0u, 0u, 0u);
           }
