@@ -63,6 +63,28 @@ def parse():
     return ap.parse_args()
 
 
+DTYPE = "f64/f32 raster, u8 RGB out"
+
+
+def workload_config(args, spec, n_links, n_tris, world):
+    """The `config` object of both arms (identical for the same args)."""
+    B = args.envs
+    return {
+        "workload": f"{args.model} ({spec.name}, {n_links} links, {n_tris} tris), {B} envs/GPU, "
+                    f"{args.mode} distractors, 84x84 {'gray' if args.grayscale else 'RGB'}",
+        "model": spec.name, "envs_per_gpu": B, "global_envs": world * B,
+        "mode": args.mode, "resolution": [84, 84], "pack_videos": args.pack_videos,
+        "parallelism": f"env-sharded x{world} (no hot-path collective)",
+    }
+
+
+def share_device() -> bool:
+    """Test hook (tests/test_bench_ranks.py): every rank on cuda:0 with the
+    gloo backend, so the multi-rank path runs on a 1-GPU box. The ranks
+    never wait on each other inside a kernel (no hot-path collective)."""
+    return os.environ.get("PXR_BENCH_SHARE_DEVICE", "") == "1"
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -164,10 +186,14 @@ def run_ours(args, world, rank, local):
     from paper_2502_00021_b200.bench_support import Workload
     from paper_2502_00021_b200.shards import aggregate, gather_stats, shard_envs
 
+    gpu = 0 if share_device() else local
     if world > 1:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        if share_device():
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     B = args.envs
     shard = shard_envs(rank, world, B)  # envs [r*B, (r+1)*B) of world*B, no hot-path collective
     from paper_2502_00021_b200.bench_support import synthetic_pack
@@ -194,7 +220,7 @@ def run_ours(args, world, rank, local):
     for t in range(max(3, args.warmup)):
         one(t)
     torch.cuda.synchronize(dev)
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(gpu)
     sampler.start()
     soak_end = time.time() + 1.0
     t_ = 0
@@ -225,10 +251,7 @@ def run_ours(args, world, rank, local):
     clocks = sampler.stop()
 
     # per-launch duration of the dominant (only) kernel inside the region
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        tdist.all_reduce(ms_t, op=tdist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = max_over_ranks(ms, dev)
     total_steps = world * B * args.steps
     value = total_steps / (ms_max / 1e3)
     per_launch_s = (ms / 1e3) / args.steps
@@ -286,22 +309,15 @@ def run_ours(args, world, rank, local):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f64/f32 raster, u8 RGB out",
+        "dtype": DTYPE,
         "data": "synthetic: on-device pose source (reference reset keys + joint oscillation, "
                 "f64 FK); " + (f"synthetic video pack ({args.pack_videos}x60x64x64, "
                                f"{pack_bytes / 2**20:.0f} MiB > 4x L2: frame fetches from HBM, "
                                "counted in the roofline bytes)" if large_pack else
                                "reference synthetic video pack (seed 2024, 4x60x64x64) in HBM"),
-        "config": {
-            "workload": f"{args.model} ({w.spec.name}, {w.n_links} links, "
-                        f"{w.geom.triangle_count} tris), {B} envs/GPU, {args.mode} distractors, "
-                        f"{w.width}x{w.height} {'gray' if args.grayscale else 'RGB'}",
-            "model": w.spec.name, "envs_per_gpu": B, "global_envs": world * B,
-            "mode": args.mode, "resolution": [w.height, w.width],
-            "parallelism": f"env-sharded x{world} (no hot-path collective)",
-            "l2": f"obs ring of {n_out} buffers ({n_out * obs_bytes / 2**20:.0f} MiB > L2) "
-                  f"+ {n_pose_sets} resident pose sets",
-        },
+        "config": workload_config(args, w.spec, w.n_links, w.geom.triangle_count, world),
+        "l2_policy": f"obs ring of {n_out} buffers ({n_out * obs_bytes / 2**20:.0f} MiB > L2) "
+                     f"+ {n_pose_sets} resident pose sets",
         "roofline": {
             "bound": "hbm",
             "achieved": achieved,
@@ -328,8 +344,22 @@ def run_ours(args, world, rank, local):
         "clocks": clocks,
     }
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(args, w, seconds=args.cpu_seconds)
+        line["cpu_baseline"] = cpu_baseline(args, seconds=args.cpu_seconds)
     return line
+
+
+def max_over_ranks(x: float, dev) -> float:
+    """MAX over ranks of a per-rank device time (NCCL on the device, or
+    gloo on the host under the shared-device test hook)."""
+    import torch
+    import torch.distributed as tdist
+
+    if not (tdist.is_available() and tdist.is_initialized()) or tdist.get_world_size() == 1:
+        return float(x)
+    on = dev if tdist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=on)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def verify_rank(args, w, shard, pack, dev):
@@ -405,10 +435,7 @@ def run_e2e(args, w, dev, world, rank):
         ends[i].record(streams[i])
     torch.cuda.synchronize(dev)
     ms = max(start.elapsed_time(e) for e in ends)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        tdist.all_reduce(ms_t, op=tdist.ReduceOp.MAX)
-    ms = float(ms_t.item())
+    ms = max_over_ranks(ms, dev)
     return {
         "value": world * B * K / (ms / 1e3),
         "unit": UNIT,
@@ -423,59 +450,103 @@ def run_e2e(args, w, dev, world, rank):
 # ---------------------------------------------------------------- CPU legs
 
 
-def _cpu_workload(w, sample_envs, n_pose_sets):
-    import numpy as np
+class HostWorkload:
+    """The same configuration as bench_support.Workload, built on the host
+    only (numpy + the C oracle; no torch, no libpxr): geometry and model
+    from the package's host-side tables (tessellation pinned by
+    tests/golden/geometry.json), poses from the host restatement of the
+    pose source (oracle.pose_source, the reference's reset keys + the same
+    joint oscillation + FK), distractor state from oracle.init_distractors
+    (distractor.py:82-113), the reference's synthetic video pack."""
 
-    poses = [w.poses(t)[:sample_envs].cpu().numpy().copy() for t in range(n_pose_sets)]
-    st = w.dist.to_host()
-    frames, starts = (w.pack.flat_frames() if w.pack is not None else (None, None))
-    return poses, {k: v[:sample_envs].copy() for k, v in st.items()}, frames, starts
+    def __init__(self, O, model, batch, mode, seed=0, env_offset=0, logical_batch=None,
+                 grayscale=False, pack_videos=4, width=84, height=84):
+        import numpy as np
+
+        from paper_2502_00021_b200.bench_support import MODEL_ALIASES, synthetic_pack
+        from paper_2502_00021_b200.models import model_kinematics, resolve_model
+        from paper_2502_00021_b200.render import RobotGeometry
+
+        self.O = O
+        self.spec = resolve_model(MODEL_ALIASES.get(model, model))
+        self.parent, self.anchor, length, radius = model_kinematics(self.spec)
+        self.geom = RobotGeometry(length, radius)
+        self.batch, self.mode, self.grayscale = int(batch), mode, bool(grayscale)
+        self.env_offset = int(env_offset)
+        self.logical_batch = int(logical_batch if logical_batch is not None else batch)
+        self.width, self.height = width, height
+        self.floor_in_background = mode == "video"  # env.py:81-85
+        self.master = O.key_from_seed(seed)
+        self.reset_key = O.fold_in(self.master, 0x5EED)
+        self.frames = self.starts = self.counts = None
+        if mode == "video":
+            pack = synthetic_pack(videos=pack_videos)
+            self.frames, self.starts = pack.flat_frames()
+            self.counts = np.asarray(pack.frame_counts, dtype=np.int64)
+        self.state = O.init_distractors(mode, self.counts, O.fold_in(self.master, 0xD157),
+                                        self.batch, env_offset=self.env_offset)
+
+    @property
+    def n_links(self):
+        return self.spec.n_links
+
+    def poses(self, t):
+        return self.O.pose_source(self.spec.rest(), self.parent, self.anchor, self.reset_key,
+                                  self.env_offset, t, self.batch)
+
+    def step(self, poses, t, threads):
+        """One rendered env-step of every env on the CPU: advance_distractors
+        (distractor.py:116-137), render_robot_batch (render.py:594-623),
+        apply_color/apply_video (distractor.py:184-214), grayscale
+        (env.py:168-173) -- the reference's per-step path."""
+        O = self.O
+        key_t = O.fold_in(self.master, t)
+        self.state = O.advance_state(self.state, self.mode, key_t, self.env_offset,
+                                     self.logical_batch, frame_counts=self.counts)
+        px, dp = O.render_robot_batch(self.geom, poses, self.width, self.height,
+                                      self.floor_in_background, threads=threads)
+        if self.mode == "color":
+            O.apply_color_inplace(px, self.state["color_bias"], threads=threads)
+        elif self.mode == "video":
+            O.apply_video_inplace(px, dp, self.frames,
+                                  self.starts[self.state["video_index"]]
+                                  + self.state["frame_cursor"], threads=threads)
+        return O.grayscale(px) if self.grayscale else px
 
 
-def _cpu_step(O, w, poses, st, frames, starts, t, threads):
-    """One reference-path step on the CPU oracle: render_robot_batch +
-    advance_distractors + apply_* (+ grayscale), render.py:594-623,
-    distractor.py:116-214, env.py:168-173."""
-    key_t = O.fold_in((w.master.hi, w.master.lo), t)
-    B = poses.shape[0]
-    px, dp = O.render_robot_batch(w.geom, poses, w.width, w.height, w.floor_in_background,
-                                  threads=threads)
-    if w.mode == "color":
-        bias = O.color_biases(key_t, w.env_offset, B)
-        O.apply_color_inplace(px, bias, threads=threads)
-    elif w.mode == "video":
-        st["frame_cursor"], st["direction"] = O.video_advance(
-            st["frame_cursor"], st["direction"], st["frame_count"])
-        O.apply_video_inplace(px, dp, frames, starts[st["video_index"]] + st["frame_cursor"],
-                              threads=threads)
-    return O.grayscale(px) if w.grayscale else px
-
-
-def cpu_baseline(args, w, seconds=10.0):
+def _oracle():
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import oracle as O
 
     O.build()
+    return O
+
+
+def cpu_baseline(args, seconds=10.0):
+    """The oracle port on all host cores, a bounded sample (~`seconds`) of
+    the same workload: full batches of args.envs envs per step."""
+    O = _oracle()
     threads = O.host_threads()
-    sample_envs = min(w.batch, 1024)
-    poses, st, frames, starts = _cpu_workload(w, sample_envs, 4)
-    _cpu_step(O, w, poses[0], st, frames, starts, 0, threads)  # warm
+    hw = HostWorkload(O, args.model, args.envs, args.mode, seed=0, grayscale=args.grayscale,
+                      pack_videos=args.pack_videos)
+    pose_sets = [hw.poses(t) for t in range(4)]
+    hw.step(pose_sets[0], 0, threads)  # warm
     n = 0
     t0 = time.perf_counter()
     while True:
-        _cpu_step(O, w, poses[n % 4], st, frames, starts, n, threads)
+        hw.step(pose_sets[n % 4], n + 1, threads)
         n += 1
         el = time.perf_counter() - t0
         if el >= seconds or n >= 10000:
             break
     return {
-        "value": n * sample_envs / el,
+        "value": n * hw.batch / el,
         "unit": UNIT,
         "cores": threads,
         "kind": "port",
-        "sample": f"{n} steps x {sample_envs} envs of the same workload ({el:.1f} s), "
-                  "C oracle (oracle/render_oracle.c: render_robot_batch + advance_distractors "
-                  "+ apply_video/apply_color), OpenMP over envs",
+        "sample": f"{n} steps x {hw.batch} envs of the same workload ({el:.1f} s): host poses, "
+                  "advance_distractors + render_robot_batch + apply_* on the C oracle "
+                  "(oracle/render_oracle.c), OpenMP over envs",
         "cpu": _cpu_model(),
     }
 
@@ -492,32 +563,26 @@ def _cpu_model():
 
 
 def run_reference(args, world, rank, local):
-    """--impl reference: the reference's CPU path (oracle port) on all host
-    cores; rank 0 only under torchrun."""
+    """--impl reference: the reference's CPU path (the C oracle port of
+    render_robot_batch + advance_distractors + apply_*; the reference is
+    Python + numba, nothing to compile into oracle/_ref) on all host cores,
+    rendering every env of the job each step (world x envs), inputs built
+    on the host. Rank 0 only under torchrun; no torch, no libpxr."""
     if rank != 0:
         return None
-    import torch
-
-    sys.path.insert(0, os.path.join(REPO, "oracle"))
-    import oracle as O
-
-    from paper_2502_00021_b200.bench_support import Workload
-
-    O.build()
+    O = _oracle()
     threads = O.host_threads()
-    dev = torch.device("cuda", local) if torch.cuda.is_available() else None
-    if dev is None:
-        return {"impl": "reference", "unavailable": "needs the workload's pose source (CUDA)"}
-    w = Workload(args.model, args.envs, args.mode, seed=0, grayscale=args.grayscale, device=dev)
-    sample_envs = min(w.batch, 512)
-    poses, st, frames, starts = _cpu_workload(w, sample_envs, 4)
+    B = args.envs * world
+    hw = HostWorkload(O, args.model, B, args.mode, seed=0, grayscale=args.grayscale,
+                      pack_videos=args.pack_videos)
+    pose_sets = [hw.poses(t) for t in range(4)]  # host-resident inputs, not timed
     for t in range(max(1, args.warmup)):
-        _cpu_step(O, w, poses[t % 4], st, frames, starts, t, threads)
+        hw.step(pose_sets[t % 4], t, threads)
     t0 = time.perf_counter()
     for k in range(args.steps):
-        _cpu_step(O, w, poses[k % 4], st, frames, starts, k, threads)
+        hw.step(pose_sets[k % 4], args.warmup + k, threads)
     el = time.perf_counter() - t0
-    value = args.steps * sample_envs / el
+    value = args.steps * B / el
     return {
         "impl": "reference",
         "metric": METRIC,
@@ -530,22 +595,38 @@ def run_reference(args, world, rank, local):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f64/f32 raster, u8 RGB out",
-        "data": "synthetic (same pose source and video pack as the GPU arm)",
-        "config": {"workload": f"{args.model} ({w.spec.name}), {args.envs} envs/GPU, "
-                               f"{args.mode} distractors, 84x84; each step renders a bounded "
-                               f"sample of {sample_envs} envs", "model": w.spec.name,
-                   "envs_per_gpu": args.envs, "mode": args.mode},
+        "dtype": DTYPE,
+        "data": "synthetic: host pose source (reference reset keys + joint oscillation, f64 FK, "
+                "numpy) and the reference synthetic video pack",
+        "config": workload_config(args, hw.spec, hw.n_links, hw.geom.triangle_count, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample_envs} envs per step, {args.steps} steps",
+                         "sample": f"every step renders all {B} envs ({args.steps} timed steps "
+                                   f"after {max(1, args.warmup)} warm-up steps)",
                          "cpu": _cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
+def self_launch(args) -> int:
+    """`--gpus N` without a torchrun environment: re-exec this script under
+    torch.distributed.run with N ranks (one process per GPU, rendezvous on
+    127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args))
     if world != args.gpus and "WORLD_SIZE" in os.environ:
         args.gpus = world
     if args.impl == "reference":

@@ -288,3 +288,124 @@ def video_advance(cursor, direction, frame_count):
     fc = np.ascontiguousarray(frame_count, dtype=np.int64)
     lib().oracle_video_advance(_p(c, _i64p), _p(d, _i8p), _p(fc, _i64p), c.size)
     return c, d
+
+
+# ---------------------------------------------------------------- host workload
+# Host-side (numpy + C oracle) restatements of the per-step glue around the
+# render path, for the full-size parity tests and the bench's reference arm.
+# No torch, no libpxr.
+
+
+def _index_from_words(w: np.ndarray, n: int) -> np.ndarray:
+    """prng.py:181-193 (32-bit halves), vectorised."""
+    w = np.asarray(w, dtype=np.uint64)
+    un = np.uint64(n)
+    hi = w >> np.uint64(32)
+    lo = w & np.uint64(0xFFFFFFFF)
+    return ((hi * un + ((lo * un) >> np.uint64(32))) >> np.uint64(32)).astype(np.int64)
+
+
+def _biases_from_keys(hi, lo) -> np.ndarray:
+    """distractor.py:66-74 _sample_biases for an array of keys."""
+    z = np.zeros_like(hi)
+    w0, w1 = threefry2x64_many(hi, lo, z, 0)
+    w2, _ = threefry2x64_many(hi, lo, z + np.uint64(1), 0)
+    out = np.empty((hi.shape[0], 3), dtype=np.int16)
+    for c, w in enumerate((w0, w1, w2)):
+        out[:, c] = _index_from_words(w, 121) - 60
+    return out
+
+
+def _video_from_keys(hi, lo, n_videos: int) -> np.ndarray:
+    """distractor.py:77-79 sample_video_indices."""
+    w0, _ = threefry2x64_many(hi, lo, np.full(hi.shape, 2, np.uint64), 0)
+    return _index_from_words(w0, n_videos)
+
+
+def init_distractors(mode: str, frame_counts, key, batch: int, env_offset: int = 0) -> dict:
+    """distractor.py:82-113: keys = split(key, off + B)[off:] (TF(key, (g, 1))),
+    colour biases / video index from each key. Returns the DistractorState
+    fields as numpy arrays (empty in mode none)."""
+    z = np.zeros(0, np.int64)
+    st = {"color_bias": np.zeros((0, 3), np.int16), "video_index": z, "frame_cursor": z.copy(),
+          "direction": np.zeros(0, np.int8), "frame_count": z.copy()}
+    if mode == "none":
+        return st
+    g = np.arange(env_offset, env_offset + batch, dtype=np.uint64)
+    hi, lo = threefry2x64_many(key[0], key[1], g, 1)
+    if mode == "color":
+        st["color_bias"] = _biases_from_keys(hi, lo)
+        return st
+    counts = np.asarray(frame_counts, dtype=np.int64)
+    vidx = _video_from_keys(hi, lo, counts.size)
+    return {"color_bias": np.zeros((batch, 3), np.int16), "video_index": vidx,
+            "frame_cursor": np.zeros(batch, np.int64), "direction": np.ones(batch, np.int8),
+            "frame_count": counts[vidx]}
+
+
+def advance_state(st: dict, mode: str, key_t, env_offset: int, logical_batch: int,
+                  frame_counts=None, done=None) -> dict:
+    """One step of the distractor state as the reference's step() does it:
+    advance_distractors (distractor.py:116-137), then for done envs the
+    video re-draw from fold_in(key_t, logical_batch + env_offset + i)
+    (env.py:226-244). Returns a new dict."""
+    out = {k: v.copy() for k, v in st.items()}
+    if mode == "color":
+        out["color_bias"] = color_biases(key_t, env_offset, st["color_bias"].shape[0])
+    elif mode == "video":
+        out["frame_cursor"], out["direction"] = video_advance(
+            st["frame_cursor"], st["direction"], st["frame_count"])
+        if done is not None and np.any(done):
+            idx = np.nonzero(np.asarray(done))[0]
+            g = np.uint64(logical_batch + env_offset) + idx.astype(np.uint64)
+            hi, lo = threefry2x64_many(key_t[0], key_t[1], g, 2)
+            counts = np.asarray(frame_counts, dtype=np.int64)
+            vidx = _video_from_keys(hi, lo, counts.size)
+            out["video_index"][idx] = vidx
+            out["frame_cursor"][idx] = 0
+            out["direction"][idx] = 1
+            out["frame_count"][idx] = counts[vidx]
+    return out
+
+
+def forward_kinematics(qpos: np.ndarray, parent, anchor) -> np.ndarray:
+    """physics.py:114-137 in numpy: per-link [x, z, pitch] chained along parents."""
+    qpos = np.asarray(qpos, dtype=np.float64)
+    nl = len(parent)
+    poses = np.zeros((qpos.shape[0], nl, 3), dtype=np.float64)
+    poses[:, 0, :] = qpos[:, :3]
+    for i in range(1, nl):
+        p = int(parent[i])
+        th = poses[:, p, 2]
+        poses[:, i, 0] = poses[:, p, 0] + anchor[i] * np.cos(th)
+        poses[:, i, 1] = poses[:, p, 1] + anchor[i] * np.sin(th)
+        poses[:, i, 2] = th + qpos[:, 3 + i - 1]
+    return poses
+
+
+def pose_source(rest, parent, anchor, reset_key, env_offset: int, t: int, batch: int):
+    """Host restatement of the benchmark pose source (csrc/pxr_ops.cu
+    pose_source_kernel): qpos0 = rest + U(-0.1, 0.1) from the reference's
+    reset keys (physics.py:499-503, prng.py:111-135), a deterministic joint
+    oscillation, then forward kinematics -- numpy f64 sin/cos, so equal to
+    the device's within a few ulp (the same workload, not the same bits)."""
+    rest = np.asarray(rest, dtype=np.float64)
+    dof = rest.size
+    g = np.arange(env_offset, env_offset + batch, dtype=np.uint64)
+    khi, klo = threefry2x64_many(reset_key[0], reset_key[1], g, 1)   # split(R, .)[g]
+    fhi, flo = threefry2x64_many(khi, klo, np.zeros(batch, np.uint64), 2)  # fold_in(k, 0)
+    q = np.empty((batch, dof), dtype=np.float64)
+    for d in range(0, dof, 2):
+        w0, w1 = threefry2x64_many(fhi, flo, np.full(batch, d // 2, np.uint64), 0)
+        for k, w in enumerate((w0, w1)):
+            if d + k < dof:
+                u = (w >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+                q[:, d + k] = rest[d + k] + (-0.1 + u * 0.2)
+    time_ = 0.01 * float(t)
+    phase = (g % np.uint64(997)).astype(np.float64) * 0.37
+    q[:, 0] += time_
+    q[:, 1] += 0.03 * np.sin(6.0 * time_ + phase)
+    q[:, 2] += 0.05 * np.sin(4.0 * time_ + phase)
+    for j in range(3, dof):
+        q[:, j] += 0.6 * np.sin(8.0 * time_ + phase + 1.3 * j)
+    return forward_kinematics(q, parent, anchor)

@@ -89,6 +89,40 @@ class TestOracleDistractor:
         np.testing.assert_array_equal(oracle.color_biases(kt, 48, 16),
                                       rec["color_adv_seed5_t3_off48_b16"])
 
+    def test_init_distractors(self, oracle):
+        """The vectorised host init (distractor.py:82-113) vs the reference's
+        outputs, with and without env_offset."""
+        rec = golden("distractor.npz")
+        k = oracle.key_from_seed(5)
+        np.testing.assert_array_equal(oracle.init_distractors("color", None, k, 64)["color_bias"],
+                                      rec["color_init_seed5_b64"])
+        np.testing.assert_array_equal(
+            oracle.init_distractors("color", None, k, 16, env_offset=48)["color_bias"],
+            rec["color_init_seed5_off48_b16"])
+        v = oracle.init_distractors("video", rec["pack_counts"], oracle.key_from_seed(9), 40,
+                                    env_offset=3)
+        np.testing.assert_array_equal(v["video_index"], rec["video_init_seed9_off3_b40"])
+        np.testing.assert_array_equal(v["frame_count"],
+                                      rec["pack_counts"][rec["video_init_seed9_off3_b40"]])
+        assert (v["frame_cursor"] == 0).all() and (v["direction"] == 1).all()
+
+    def test_pose_source_host(self, oracle):
+        """The host pose source: reset draws within rest +- 0.1 at t=0 for the
+        root, FK chained along parents, env_offset slices consistent."""
+        from paper_2502_00021_b200.models import model_kinematics
+
+        spec = spec_of("humanoid_lite")
+        par, anc, _, _ = model_kinematics(spec)
+        rk = oracle.fold_in(oracle.key_from_seed(0), 0x5EED)
+        full = oracle.pose_source(spec.rest(), par, anc, rk, 0, 7, 64)
+        part = oracle.pose_source(spec.rest(), par, anc, rk, 40, 7, 8)
+        np.testing.assert_array_equal(full[40:48], part)
+        assert full.shape == (64, spec.n_links, 3)
+        t0 = oracle.pose_source(spec.rest(), par, anc, rk, 0, 0, 64)
+        g = np.arange(64) % 997 * 0.37
+        base = t0[:, 0, 1] - 0.03 * np.sin(g)
+        assert np.all(np.abs(base - spec.rest()[1]) <= 0.1 + 1e-12)
+
     def test_ping_pong(self, oracle):
         rec = golden("distractor.npz")
         seq, dirs = rec["video_cursor_seq"], rec["video_dir_seq"]
@@ -125,37 +159,24 @@ def oracle_replay(oracle, tag, steps=None):
     master = oracle.key_from_seed(m["seed"])
     dist_key = oracle.fold_in(master, 0xD157)
     n = rec["poses"].shape[0] if steps is None else steps + 1
+    frames = starts = counts = None
     if m["mode"] == "video":
         frames, starts, counts = rec["pack_frames"], rec["pack_starts"], rec["pack_counts"]
-        nvid = len(counts)
-        vidx = np.array([oracle.video_index_for_key(oracle.split_one(dist_key, off + i), nvid)
-                         for i in range(B)], dtype=np.int64)
-        cur = np.zeros(B, np.int64)
-        dirs = np.ones(B, np.int8)
-    elif m["mode"] == "color":
-        keys = [oracle.split_one(dist_key, off + i) for i in range(B)]
-        bias = np.array([[oracle.index_from_word(w, 121) - 60 for w in (
-            oracle.threefry2x64(*k, 0, 0)[0], oracle.threefry2x64(*k, 0, 0)[1],
-            oracle.threefry2x64(*k, 1, 0)[0])] for k in keys], dtype=np.int16)
+    # the vectorised host restatements (oracle.init_distractors /
+    # advance_state) pinned here by the reference's own hash chains
+    st = oracle.init_distractors(m["mode"], counts, dist_key, B, env_offset=off)
     h = b"\x00" * 32
     for t in range(n):
         if t > 0:
-            key_t = oracle.fold_in(master, t - 1)
-            if m["mode"] == "color":
-                bias = oracle.color_biases(key_t, off, B)
-            elif m["mode"] == "video":
-                cur, dirs = oracle.video_advance(cur, dirs, counts[vidx])
-                for i in np.nonzero(rec["done"][t])[0]:
-                    r = oracle.fold_in(key_t, lb + off + int(i))
-                    vidx[i] = oracle.video_index_for_key(r, nvid)
-                    cur[i] = 0
-                    dirs[i] = 1
+            st = oracle.advance_state(st, m["mode"], oracle.fold_in(master, t - 1), off, lb,
+                                      frame_counts=counts, done=rec["done"][t])
         px, dp = oracle.render_robot_batch(geom, rec["poses"][t], 84, 84,
                                            m["floor_in_background"], threads=4)
         if m["mode"] == "color":
-            oracle.apply_color_inplace(px, bias)
+            oracle.apply_color_inplace(px, st["color_bias"])
         elif m["mode"] == "video":
-            oracle.apply_video_inplace(px, dp, frames, starts[vidx] + cur)
+            oracle.apply_video_inplace(px, dp, frames,
+                                       starts[st["video_index"]] + st["frame_cursor"])
         obs = oracle.grayscale(px) if m["observation"] == "grayscale" else px
         h = hashlib.sha256(h + np.ascontiguousarray(obs).tobytes()).digest()
         assert h == rec["hashes"][t].tobytes(), f"{tag}: oracle diverges at t={t}"
