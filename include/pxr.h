@@ -109,6 +109,11 @@ int32_t pxr_build_checked(void);
 const char *pxr_status_string(pxr_status s);
 /* Last CUDA error string seen by a failing call (thread-local). */
 const char *pxr_last_error(void);
+/* Test / debug knobs (no reference counterpart): `name` is one of
+ * PXR_DEBUG_FRAG_LIMIT, _ROW_CAP, _CAP, _STATS_PTR, _BAND_H, _NO_PACKED_SCAN,
+ * _PHYS, _RENDER; `value` its string value, NULL to unset. The PXR_DEBUG_*
+ * environment is read once at the first query; this overrides it. */
+pxr_status pxr_set_debug(const char *name, const char *value);
 
 /* Floor ray-direction table for a camera block: f64 (H, W, 3), the exact
  * incremental sequence of render.py:316-344. Writes `*separable` (host). */

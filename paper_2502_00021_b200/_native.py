@@ -32,7 +32,7 @@ EXPORTED = (
     "pxr_apply_color", "pxr_apply_video", "pxr_grayscale", "pxr_threefry2x64",
     "pxr_sincosf", "pxr_pose_source", "pxr_forward_kinematics", "pxr_div_check",
     "pxr_physics_step", "pxr_reset_envs", "pxr_env_poses", "pxr_conv_stub_forward",
-    "pxr_step_key_advance",
+    "pxr_step_key_advance", "pxr_set_debug",
 )
 
 _vp = ctypes.c_void_p
@@ -159,6 +159,8 @@ def lib() -> ctypes.CDLL:
     L.pxr_step_key_advance.argtypes = [_u64, _u64, _vp, _vp, _vp]
     L.pxr_env_poses.restype = _i32
     L.pxr_env_poses.argtypes = [P(Model), _vp, _i64, _vp, _vp]
+    L.pxr_set_debug.restype = _i32
+    L.pxr_set_debug.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
     if L.pxr_abi_version() != 2:
         raise ImportError(f"{LIB_PATH}: ABI version {L.pxr_abi_version()} != 2")
     _lib = L
@@ -175,6 +177,13 @@ def check(status: int) -> None:
     raise NativeError(f"{lib().pxr_status_string(status).decode()}: {msg}")
 
 
+def set_debug(name: str, value) -> None:
+    """Set (or, with None, unset) a PXR_DEBUG_* knob of the loaded library
+    (forced raster budgets / bands / kernel variants for the tests). The
+    library reads the environment once; this is the run-time override."""
+    check(lib().pxr_set_debug(name.encode(), None if value is None else str(value).encode()))
+
+
 def require_cuda():
     """The device the kernels run on; raises when there is none."""
     import torch
@@ -185,6 +194,14 @@ def require_cuda():
             "available and there is no CPU fallback"
         )
     return torch.device("cuda", torch.cuda.current_device())
+
+
+def device_scope(device):
+    """Make ``device`` current for the launches inside (kernels go to that
+    device's current stream; the library's per-device launch facts follow)."""
+    import torch
+
+    return torch.cuda.device(device)
 
 
 def stream_ptr(stream=None) -> int:

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/pxr.h"
 
@@ -39,6 +40,40 @@ inline pxr_status set_unsupported(const char *msg) {
   return PXR_ERR_UNSUPPORTED;
 }
 pxr_status set_cuda(cudaError_t e, const char *where);
+
+// Debug / test knobs (forced raster budgets, row bands, physics variant,
+// workload counters). Read from the PXR_DEBUG_* environment once, at the
+// first query; pxr_set_debug() changes them at run time (the tests). Never
+// consulted per element: the launch paths read them once per call.
+enum DebugKnob {
+  kDbgFragLimit,     // PXR_DEBUG_FRAG_LIMIT: fragment list limit
+  kDbgRowCap,        // PXR_DEBUG_ROW_CAP: bbox rows per raster round
+  kDbgCap,           // PXR_DEBUG_CAP: live-triangle records per round
+  kDbgStatsPtr,      // PXR_DEBUG_STATS_PTR: device int32 workload counters
+  kDbgBandH,         // PXR_DEBUG_BAND_H: rows per band
+  kDbgNoPackedScan,  // PXR_DEBUG_NO_PACKED_SCAN: two-scan block scan
+  kDbgPhys,          // PXR_DEBUG_PHYS: warp|half|quarter|thread physics kernel
+  kDbgRender,        // PXR_DEBUG_RENDER: legacy|pipe|split render kernel
+  kDbgCount
+};
+// value of a knob, or nullptr when unset
+const char *debug_knob(int id);
+inline int64_t debug_int(int id, int64_t dflt) {
+  const char *s = debug_knob(id);
+  return s != nullptr ? (int64_t)strtoll(s, nullptr, 0) : dflt;
+}
+
+// Per-device launch facts, queried once per device: SM count and the opt-in
+// shared memory per block.
+struct DeviceFacts {
+  int device, num_sms, max_smem_optin;
+};
+const DeviceFacts &device_facts();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) + occupancy query for
+// (kernel, device, smem), cached: the first launch of a configuration pays
+// for the driver calls, later launches only look the answer up.
+pxr_status kernel_occupancy(const void *kernel, int threads, int smem, int *per_sm);
 
 inline pxr_status check_launch(const char *where) {
   cudaError_t e = cudaGetLastError();

@@ -12,6 +12,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/pxr.h"
 #include "pxr_internal.cuh"
@@ -28,6 +34,85 @@ void set_last_error(const char *msg) {
 pxr_status set_cuda(cudaError_t e, const char *where) {
   snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, cudaGetErrorString(e));
   return PXR_ERR_CUDA;
+}
+
+// ---- debug knobs ------------------------------------------------------------
+static const char *const kKnobNames[kDbgCount] = {
+    "PXR_DEBUG_FRAG_LIMIT", "PXR_DEBUG_ROW_CAP",        "PXR_DEBUG_CAP",  "PXR_DEBUG_STATS_PTR",
+    "PXR_DEBUG_BAND_H",     "PXR_DEBUG_NO_PACKED_SCAN", "PXR_DEBUG_PHYS", "PXR_DEBUG_RENDER"};
+static std::mutex g_knob_mu;
+static std::string g_knob_val[kDbgCount];
+static bool g_knob_set[kDbgCount];
+static bool g_knob_init = false;
+
+static void knobs_init_locked() {
+  if (g_knob_init) return;
+  for (int i = 0; i < kDbgCount; i++) {
+    const char *s = getenv(kKnobNames[i]);
+    g_knob_set[i] = s != nullptr;
+    g_knob_val[i] = s != nullptr ? s : "";
+  }
+  g_knob_init = true;
+}
+
+const char *debug_knob(int id) {
+  std::lock_guard<std::mutex> g(g_knob_mu);
+  knobs_init_locked();
+  return g_knob_set[id] ? g_knob_val[id].c_str() : nullptr;
+}
+
+// ---- per-device facts and the launch-configuration cache ------------------
+static std::mutex g_dev_mu;
+static DeviceFacts g_dev[64];
+static bool g_dev_ok[64];
+
+const DeviceFacts &device_facts() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  if (!g_dev_ok[dev]) {
+    DeviceFacts f{dev, 0, 0};
+    cudaDeviceGetAttribute(&f.num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&f.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (f.num_sms <= 0) f.num_sms = 148;
+    g_dev[dev] = f;
+    g_dev_ok[dev] = true;
+  }
+  return g_dev[dev];
+}
+
+struct OccEntry {
+  const void *kernel;
+  int device, threads, smem, per_sm;
+};
+static std::vector<OccEntry> g_occ;
+static std::vector<std::pair<std::pair<const void *, int>, int>> g_attr;  // (kernel, dev) -> smem set
+
+pxr_status kernel_occupancy(const void *kernel, int threads, int smem, int *per_sm) {
+  const int dev = device_facts().device;
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  for (const OccEntry &e : g_occ)
+    if (e.kernel == kernel && e.device == dev && e.threads == threads && e.smem == smem) {
+      *per_sm = e.per_sm;
+      return PXR_OK;
+    }
+  int *set = nullptr;
+  for (auto &a : g_attr)
+    if (a.first.first == kernel && a.first.second == dev) set = &a.second;
+  if (set == nullptr || *set < smem) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
+    if (set != nullptr) *set = smem;
+    else g_attr.push_back({{kernel, dev}, smem});
+  }
+  int n = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
+  if (e != cudaSuccess) return set_cuda(e, "occupancy query");
+  if (n < 1) n = 1;
+  g_occ.push_back({kernel, dev, threads, smem, n});
+  *per_sm = n;
+  return PXR_OK;
 }
 
 static inline unsigned blocks_for(int64_t n, int threads) {
@@ -261,6 +346,19 @@ extern "C" const char *pxr_status_string(pxr_status s) {
 }
 
 extern "C" const char *pxr_last_error(void) { return g_last_error; }
+
+extern "C" pxr_status pxr_set_debug(const char *name, const char *value) {
+  if (name == nullptr) return set_invalid("pxr_set_debug: null name");
+  std::lock_guard<std::mutex> g(g_knob_mu);
+  knobs_init_locked();
+  for (int i = 0; i < kDbgCount; i++)
+    if (strcmp(name, kKnobNames[i]) == 0) {
+      g_knob_set[i] = value != nullptr;
+      g_knob_val[i] = value != nullptr ? value : "";
+      return PXR_OK;
+    }
+  return set_invalid("pxr_set_debug: unknown knob");
+}
 
 extern "C" pxr_status pxr_init_distractors(const pxr_distractor *dist,
                                            const pxr_video_pack *pack, int64_t batch,

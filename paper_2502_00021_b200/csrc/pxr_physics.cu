@@ -683,7 +683,7 @@ extern "C" pxr_status pxr_physics_step(const pxr_model *model, double *qpos, dou
   a.ep_len = model->episode_length;
   // sub-warp kernels in the latency-bound range, one thread per env above
   // (throughput); PXR_DEBUG_PHYS=warp|half|quarter|thread forces one
-  const char *force = getenv("PXR_DEBUG_PHYS");
+  const char *force = debug_knob(kDbgPhys);
   const int nd = model->n_links + 2;
   char kind = batch <= kWarpEnvMax                  ? 'w'
               : batch <= kHalfEnvMax                  ? 'h'

@@ -360,20 +360,30 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   const int smem = use_fb ? with_table + ((2 * frame + 15) & ~15) : with_table;
   if (smem > 220 * 1024) return set_unsupported("observation too large for the policy kernel");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaFuncSetAttribute(conv_feat_tc_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
-  // the full shared-memory carveout (frames + bf16 frame + operands)
-  e = cudaFuncSetAttribute(conv_feat_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           100);
-  if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // the full shared-memory carveout (frames + bf16 frame + operands), set
+  // once per device; the dynamic-smem attribute through the launch cache
+  const DeviceFacts &df = device_facts();
+  static bool carveout_set[64] = {};
+  if (!carveout_set[df.device & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(conv_feat_tc_kernel,
+                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
+    carveout_set[df.device & 63] = true;
+  }
+  int per_sm = 0;
+  {
+    const pxr_status os = kernel_occupancy((const void *)conv_feat_tc_kernel, kTcThreads, smem,
+                                           &per_sm);
+    if (os != PXR_OK) return os;
+  }
+  const int sms = df.num_sms;
   // CTAs per SM from the shared memory per SM (the occupancy query does not
   // see the carveout preference set above)
-  int smem_sm = 0;
-  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  static int smem_sm_dev[64] = {};
+  if (smem_sm_dev[df.device & 63] == 0)
+    cudaDeviceGetAttribute(&smem_sm_dev[df.device & 63], cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                           df.device);
+  const int smem_sm = smem_sm_dev[df.device & 63];
   per_sm = smem_sm / (smem + 2048);
   if (per_sm > 2048 / kTcThreads) per_sm = 2048 / kTcThreads;
   if (per_sm < 1) per_sm = 1;
@@ -397,9 +407,10 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
     case 28: pk = conv_proj_kernel<28>; break;
     default: pk = conv_proj_kernel<32>; break;
   }
-  per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk, kProjEnvs * 32, psmem);
-  if (per_sm < 1) per_sm = 1;
+  {
+    const pxr_status os = kernel_occupancy((const void *)pk, kProjEnvs * 32, psmem, &per_sm);
+    if (os != PXR_OK) return os;
+  }
   cap = (int64_t)sms * per_sm;
   const int64_t groups = (batch + kProjEnvs - 1) / kProjEnvs;
   grid = (int)(groups < cap ? groups : cap);

@@ -1356,18 +1356,6 @@ __global__ void div_check_kernel(const double *a, const double *b, double *q_pre
   }
 }
 
-static int g_num_sms = 0;
-
-static int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
-
 }  // namespace pxr
 
 using namespace pxr;
@@ -1491,29 +1479,26 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
                 ((reinterpret_cast<uintptr_t>(out_depth) & 15) == 0);
   p.frame_bytes = (int)(npx64 * C);
   p.use_bulk = (p.frame_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(out_obs) & 15) == 0);
-  // Test hooks (tests/test_gpu_parity.py): shrink the per-round budgets so
-  // the multi-round and fragment-overflow paths run on small inputs.
+  // Test hooks (tests/test_gpu_parity.py, pxr_set_debug): shrink the
+  // per-round budgets so the multi-round and fragment-overflow paths run on
+  // small inputs.
   p.frag_limit = kFragCap;
   p.row_cap = kRowCap > p.H ? kRowCap : p.H;
-  int debug_cap = 0;
-  if (const char *s = getenv("PXR_DEBUG_FRAG_LIMIT")) {
-    const int v = atoi(s);
-    if (v >= 0 && v < kFragCap) p.frag_limit = v;
+  {
+    const int64_t v = debug_int(kDbgFragLimit, -1);
+    if (v >= 0 && v < kFragCap) p.frag_limit = (int)v;
   }
-  if (const char *s = getenv("PXR_DEBUG_ROW_CAP")) {
-    const int v = atoi(s);
-    if (v > 0) p.row_cap = v > p.H ? v : p.H;
+  {
+    const int64_t v = debug_int(kDbgRowCap, 0);
+    if (v > 0) p.row_cap = v > p.H ? (int)v : p.H;
   }
-  if (const char *s = getenv("PXR_DEBUG_CAP")) debug_cap = atoi(s);
-  // debug: a device int32 (batch, 7) buffer for per-env workload counters
-  if (const char *s = getenv("PXR_DEBUG_STATS_PTR")) p.stats = (int32_t *)strtoull(s, nullptr, 0);
-  int debug_band = 0;
-  if (const char *s = getenv("PXR_DEBUG_BAND_H")) debug_band = atoi(s);
+  const int debug_cap = (int)debug_int(kDbgCap, 0);
+  // debug: a device int32 (batch, kStats) buffer for per-env workload counters
+  p.stats = (int32_t *)(uintptr_t)debug_int(kDbgStatsPtr, 0);
+  const int debug_band = (int)debug_int(kDbgBandH, 0);
 
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int max_optin = 0;
-  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const DeviceFacts &dev = device_facts();
+  const int max_optin = dev.max_smem_optin;
   const int budget =
       max_optin - (int)(sizeof(EnvShared) + sizeof(DistSlot) * 32 + 8 * kWarps) - 256;
   // Live-triangle records per round: all triangles if they fit, else the
@@ -1550,7 +1535,7 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     int rb = 0, lb = 0;
     while (rb < 32 && ((int64_t)1 << rb) <= (int64_t)p.nt * p.band_h) rb++;
     while (lb < 32 && ((int64_t)1 << lb) <= (int64_t)p.nt) lb++;
-    p.scan_sh = (rb + lb <= 32 && rb < 32 && !getenv("PXR_DEBUG_NO_PACKED_SCAN")) ? rb : 0;
+    p.scan_sh = (rb + lb <= 32 && rb < 32 && debug_knob(kDbgNoPackedScan) == nullptr) ? rb : 0;
   }
   const int smem = smem_layout(p).total;
   if (smem > budget) return set_unsupported("frame too large for one CTA's shared memory");
@@ -1559,13 +1544,10 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
                                        : render_step_kernel<true, false>)
                        : (p.draw_floor ? render_step_kernel<false, true>
                                        : render_step_kernel<false, false>);
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return set_cuda(e, "cudaFuncSetAttribute");
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
-  if (e != cudaSuccess) return set_cuda(e, "occupancy query");
-  if (per_sm < 1) per_sm = 1;
-  int64_t grid = (int64_t)num_sms() * per_sm;
+  int per_sm = 1;
+  const pxr_status os = kernel_occupancy((const void *)kernel, kThreads, smem, &per_sm);
+  if (os != PXR_OK) return os;
+  int64_t grid = (int64_t)dev.num_sms * per_sm;
   if (grid > batch) grid = batch;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   kernel<<<(unsigned)grid, kThreads, smem, st>>>(p);

@@ -298,6 +298,9 @@ class RobotRenderer:
         if width < 8 or height < 8:
             raise ValueError("frames must be at least 8x8")
         self.device = device if device is not None else _native.require_cuda()
+        self.device = torch.device(self.device)
+        if self.device.index is None:  # "cuda" -> the current device, explicitly
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.geom = geom
         self.width, self.height = int(width), int(height)
         self.cam_config = cam_config
@@ -327,6 +330,16 @@ class RobotRenderer:
 
         if poses.dtype != torch.float64 or poses.device.type != "cuda":
             raise ValueError("poses must be a float64 CUDA tensor")
+        if torch.device(poses.device) != torch.device(self.device):
+            raise ValueError(f"poses are on {poses.device}, the renderer on {self.device}")
+        with _native.device_scope(self.device):
+            return self._render(poses, floor_in_background, dist, pack, advance, keys, done,
+                                grayscale, out_obs, out_depth, want_depth, stream)
+
+    def _render(self, poses, floor_in_background, dist, pack, advance, keys, done, grayscale,
+                out_obs, out_depth, want_depth, stream):
+        import torch
+
         poses = poses.contiguous()
         B = int(poses.shape[0])
         if poses.dim() != 3 or poses.shape[1] != self.geom.n_links or poses.shape[2] != 3:

@@ -94,3 +94,31 @@ def pkg():
 
     P._native.lib()
     return P
+
+
+class _Knobs:
+    """PXR_DEBUG_* knobs of the loaded library (pxr_set_debug), unset again
+    at teardown."""
+
+    def __init__(self):
+        self._set = []
+
+    def set(self, name, value):
+        from paper_2502_00021_b200 import _native
+
+        _native.set_debug(name, value)
+        self._set.append(name)
+
+    def clear(self):
+        from paper_2502_00021_b200 import _native
+
+        for name in reversed(self._set):
+            _native.set_debug(name, None)
+        self._set.clear()
+
+
+@pytest.fixture
+def knobs():
+    k = _Knobs()
+    yield k
+    k.clear()

@@ -15,11 +15,11 @@ FIELDS = ("color_bias", "video_index", "frame_cursor", "direction", "frame_count
     ("Humanoid", "video", False, 0), ("Ant", "color", True, 0),
     ("HalfCheetah", "none", False, 0), ("Walker2d", "video", False, 28),
 ])
-def test_repeated_steps_are_bitwise_identical(torch, monkeypatch, model, mode, gray, band):
+def test_repeated_steps_are_bitwise_identical(torch, knobs, model, mode, gray, band):
     from paper_2502_00021_b200.bench_support import Workload
 
     if band:
-        monkeypatch.setenv("PXR_DEBUG_BAND_H", str(band))
+        knobs.set("PXR_DEBUG_BAND_H", str(band))
     w = Workload(model, 2048, mode, seed=5, grayscale=gray)
     done = torch.zeros(w.batch, dtype=torch.uint8, device="cuda")
     for t in range(0, 240, 12):

@@ -32,10 +32,10 @@ def _case(seed):
 
 # PXR_FUZZ_SEEDS=N widens the sweep for soak runs (default 40)
 @pytest.mark.parametrize("seed", range(int(os.environ.get("PXR_FUZZ_SEEDS", "40"))))
-def test_fused_render_fuzz_vs_oracle(pkg, torch, oracle, monkeypatch, seed):
+def test_fused_render_fuzz_vs_oracle(pkg, torch, oracle, knobs, seed):
     rng, name, mode, H, W, band, offset, fov, fib, gray, hv, wv = _case(seed)
     if band:
-        monkeypatch.setenv("PXR_DEBUG_BAND_H", str(band))
+        knobs.set("PXR_DEBUG_BAND_H", str(band))
     from paper_2502_00021_b200.models import forward_kinematics_host
 
     spec = spec_of(name)

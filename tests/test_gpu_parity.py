@@ -113,11 +113,11 @@ class TestRenderGolden:
         {"PXR_DEBUG_BAND_H": "7", "PXR_DEBUG_CAP": "40"},  # bands + rounds, plain stores
         {"PXR_DEBUG_NO_PACKED_SCAN": "1", "PXR_DEBUG_CAP": "40"},  # two-scan block scan
     ])
-    def test_round_and_overflow_paths_exact(self, torch, pkg, monkeypatch, knobs):
+    def test_round_and_overflow_paths_exact(self, torch, pkg, knobs):
         """The multi-round and fragment-overflow paths (only reached by large
         meshes / frames at default budgets) forced on the golden frames."""
         for k, v in knobs.items():
-            monkeypatch.setenv(k, v)
+            knobs.set(k, v)
         for name in ("humanoid_lite", "cheetah_lite"):
             rec = golden(f"render_{name}.npz")
             geom = geometry_of(name)
@@ -293,10 +293,10 @@ def test_fused_replay_hash_chain(torch, pkg, tag):
 
 @pytest.mark.parametrize("tag,band", [("walker_video_b8", "12"), ("hopper_color_gray_b4", "5"),
                                       ("humanoid_video_b8_slice", "32")])
-def test_fused_replay_hash_chain_banded(torch, pkg, monkeypatch, tag, band):
+def test_fused_replay_hash_chain_banded(torch, pkg, knobs, tag, band):
     """The same chains with the frame forced into row bands (the path large
     frames take): per-band raster, composite, grayscale and store."""
-    monkeypatch.setenv("PXR_DEBUG_BAND_H", band)
+    knobs.set("PXR_DEBUG_BAND_H", band)
     fused_replay(torch, pkg, tag)
 
 

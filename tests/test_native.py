@@ -117,3 +117,14 @@ def test_cpu_has_no_fallback(native, monkeypatch):
     with pytest.raises(RuntimeError):
         P.render_robot_batch(P.RobotGeometry([0.5], [0.05]), [[[0.0, 0.6, 0.0]]],
                              P.CameraConfig(), 84, 84, False)
+
+
+def test_debug_knobs_set_and_unset(native):
+    """pxr_set_debug: the run-time override of the PXR_DEBUG_* environment
+    (read once by the library); unknown names are a ValueError."""
+    from paper_2502_00021_b200 import _native
+
+    _native.set_debug("PXR_DEBUG_BAND_H", 12)
+    _native.set_debug("PXR_DEBUG_BAND_H", None)
+    with pytest.raises(ValueError):
+        _native.set_debug("PXR_DEBUG_NOT_A_KNOB", 1)

@@ -68,7 +68,7 @@ class TestPhysicsAPI:
             pkg.step_dynamics(spec, st, act[:, :-1] if act.shape[1] else np.zeros((32, 1)))
 
     @pytest.mark.parametrize("name", MODEL_NAMES)
-    def test_warp_and_thread_kernels_agree_bitwise(self, pkg, torch, monkeypatch, name):
+    def test_warp_and_thread_kernels_agree_bitwise(self, pkg, torch, knobs, name):
         """pxr_physics_step has warp-per-env and half-warp-per-env kernels
         (small / medium batches) and a thread-per-env kernel (large); the same
         env must step
@@ -81,7 +81,7 @@ class TestPhysicsAPI:
         acts = rng.uniform(-1.5, 1.5, (60,) + rec[f"{name}_act"].shape)
         finals = []
         for kind in ("warp", "thread", "half", "quarter"):
-            monkeypatch.setenv("PXR_DEBUG_PHYS", kind)
+            knobs.set("PXR_DEBUG_PHYS", kind)
             st = pkg.SystemState(torch.from_numpy(rec[f"{name}_qpos"]).cuda(),
                                  torch.from_numpy(rec[f"{name}_qvel"]).cuda(),
                                  torch.from_numpy(rec[f"{name}_steps"]).cuda(),

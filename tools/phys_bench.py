@@ -13,7 +13,7 @@ for model in ("humanoid_lite", "cheetah_lite"):
         act = torch.zeros((B, env.n_joints), dtype=torch.float64, device='cuda')
         res = []
         for kind in ("thread", "warp", "half", "quarter"):
-            os.environ["PXR_DEBUG_PHYS"] = kind
+            _native.set_debug("PXR_DEBUG_PHYS", kind)
             sysc = s.sys.copy(); rew = torch.zeros(B, dtype=torch.float64, device='cuda')
             f = lambda: L.pxr_physics_step(ctypes.byref(env.model_c), sysc.qpos.data_ptr(), sysc.qvel.data_ptr(), sysc.step_count.data_ptr(), sysc.done.data_ptr(), act.data_ptr(), rew.data_ptr(), B, _native.stream_ptr())
             for _ in range(3): f()

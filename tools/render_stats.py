@@ -29,12 +29,13 @@ ap.add_argument("--mode", default="video")
 ap.add_argument("--step", type=int, default=3)
 ap.add_argument("--size", type=int, nargs=2, default=(84, 84), metavar=("H", "W"))
 a = ap.parse_args()
+from paper_2502_00021_b200 import _native
 w = Workload(a.model, a.envs, a.mode, height=a.size[0], width=a.size[1])
 stats = torch.full((a.envs, len(NAMES)), -1, dtype=torch.int32, device="cuda")
-os.environ["PXR_DEBUG_STATS_PTR"] = str(stats.data_ptr())
+_native.set_debug("PXR_DEBUG_STATS_PTR", stats.data_ptr())
 w.render(w.poses(a.step), a.step)
 torch.cuda.synchronize()
-del os.environ["PXR_DEBUG_STATS_PTR"]
+_native.set_debug("PXR_DEBUG_STATS_PTR", None)
 st = stats.cpu().numpy()
 assert (st >= 0).all(), "stats not written for every env"
 print(f"{a.model} {a.mode} {a.size[0]}x{a.size[1]} B={a.envs} step {a.step}")
