@@ -89,8 +89,15 @@ class TestDeviceMath:
 
 
 class TestRenderGolden:
+    @pytest.mark.parametrize("variant", ["auto", "legacy", "pipe"])
     @pytest.mark.parametrize("name", MODEL_NAMES)
-    def test_frames_exact(self, torch, pkg, name):
+    def test_frames_exact(self, torch, pkg, knobs, name, variant):
+        """Golden frames through each render kernel: the default dispatch,
+        and each kernel forced with at most 3 CTAs (so every CTA renders
+        several envs: the cross-env prefetch / the two-stage pipeline)."""
+        if variant != "auto":
+            knobs.set("PXR_DEBUG_RENDER", variant)
+            knobs.set("PXR_DEBUG_GRID", 3)
         rec = golden(f"render_{name}.npz")
         geom = geometry_of(name)
         poses = to_dev(torch, rec["poses"])
@@ -104,7 +111,7 @@ class TestRenderGolden:
         np.testing.assert_array_equal(fr.depth.cpu().numpy().view(np.uint32),
                                       rec["depth_64x48"].view(np.uint32))
 
-    @pytest.mark.parametrize("knobs", [
+    @pytest.mark.parametrize("kv", [
         {"PXR_DEBUG_CAP": "40"},                       # many record rounds
         {"PXR_DEBUG_ROW_CAP": "90"},                   # many bbox-row rounds
         {"PXR_DEBUG_FRAG_LIMIT": "16"},                # fragment-list overflow path
@@ -113,10 +120,14 @@ class TestRenderGolden:
         {"PXR_DEBUG_BAND_H": "7", "PXR_DEBUG_CAP": "40"},  # bands + rounds, plain stores
         {"PXR_DEBUG_NO_PACKED_SCAN": "1", "PXR_DEBUG_CAP": "40"},  # two-scan block scan
     ])
-    def test_round_and_overflow_paths_exact(self, torch, pkg, knobs):
+    @pytest.mark.parametrize("variant", ["legacy", "pipe"])
+    def test_round_and_overflow_paths_exact(self, torch, pkg, knobs, kv, variant):
         """The multi-round and fragment-overflow paths (only reached by large
-        meshes / frames at default budgets) forced on the golden frames."""
-        for k, v in knobs.items():
+        meshes / frames at default budgets) forced on the golden frames, for
+        both render kernels (the pipeline with several envs per CTA)."""
+        knobs.set("PXR_DEBUG_RENDER", variant)
+        knobs.set("PXR_DEBUG_GRID", 3)
+        for k, v in kv.items():
             knobs.set(k, v)
         for name in ("humanoid_lite", "cheetah_lite"):
             rec = golden(f"render_{name}.npz")
@@ -286,8 +297,12 @@ def fused_replay(torch, pkg, tag):
         np.testing.assert_array_equal(host["direction"], rec["final_direction"])
 
 
+@pytest.mark.parametrize("variant", ["auto", "legacy", "pipe"])
 @pytest.mark.parametrize("tag", REPLAYS)
-def test_fused_replay_hash_chain(torch, pkg, tag):
+def test_fused_replay_hash_chain(torch, pkg, knobs, tag, variant):
+    if variant != "auto":
+        knobs.set("PXR_DEBUG_RENDER", variant)
+        knobs.set("PXR_DEBUG_GRID", 3)
     fused_replay(torch, pkg, tag)
 
 
