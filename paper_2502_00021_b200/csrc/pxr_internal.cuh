@@ -53,9 +53,7 @@ enum DebugKnob {
   kDbgBandH,         // PXR_DEBUG_BAND_H: rows per band
   kDbgNoPackedScan,  // PXR_DEBUG_NO_PACKED_SCAN: two-scan block scan
   kDbgPhys,          // PXR_DEBUG_PHYS: warp|half|quarter|thread physics kernel
-  kDbgRender,        // PXR_DEBUG_RENDER: legacy|pipe render kernel
   kDbgGrid,          // PXR_DEBUG_GRID: at most this many CTAs (several envs per CTA)
-  kDbgPipeProf,      // PXR_DEBUG_PIPE_PROF: device int64 (grid, 16) stage cycle counters
   kDbgCount
 };
 // value of a knob, or nullptr when unset

@@ -34,15 +34,7 @@ CONFIGS = [
     ("Walker2d", 4096, "video", True),     # grayscale composite
     ("Ant", 4096, "color", True),
 ]
-# the default dispatch takes the warp-specialised pipeline at these sizes;
-# these run the same checks through the one-env-at-a-time kernel
-LEGACY = [
-    ("Ant", 1024, "color", False),
-    ("Humanoid", 4096, "video", False),
-    ("HalfCheetah", 16384, "none", False),
-    ("Walker2d", 4096, "video", True),
-]
-CASES = [c + ("auto",) for c in CONFIGS] + [c + ("legacy",) for c in LEGACY]
+CASES = CONFIGS
 
 STEPS = 3
 DONE_RATE = 0.15
@@ -70,13 +62,10 @@ def _first_bad_env(a, b):
     return bad[:10]
 
 
-@pytest.mark.parametrize("model,B,mode,gray,variant", CASES,
-                         ids=[f"{m}-{b}-{d}{'-gray' if g else ''}-{v}" for m, b, d, g, v in CASES])
-def test_fused_step_full_batch(torch, pkg, oracle, knobs, model, B, mode, gray, variant):
+@pytest.mark.parametrize("model,B,mode,gray", CASES,
+                         ids=[f"{m}-{b}-{d}{'-gray' if g else ''}" for m, b, d, g in CASES])
+def test_fused_step_full_batch(torch, pkg, oracle, model, B, mode, gray):
     from paper_2502_00021_b200 import bench_support as bs
-
-    if variant != "auto":
-        knobs.set("PXR_DEBUG_RENDER", variant)
 
     seed = 11
     w = bs.Workload(model, B, mode, seed=seed, grayscale=gray)

@@ -89,15 +89,15 @@ class TestDeviceMath:
 
 
 class TestRenderGolden:
-    @pytest.mark.parametrize("variant", ["auto", "legacy", "pipe"])
+    @pytest.mark.parametrize("grid", [0, 3])
     @pytest.mark.parametrize("name", MODEL_NAMES)
-    def test_frames_exact(self, torch, pkg, knobs, name, variant):
-        """Golden frames through each render kernel: the default dispatch,
-        and each kernel forced with at most 3 CTAs (so every CTA renders
-        several envs: the cross-env prefetch / the two-stage pipeline)."""
-        if variant != "auto":
-            knobs.set("PXR_DEBUG_RENDER", variant)
-            knobs.set("PXR_DEBUG_GRID", 3)
+    def test_frames_exact(self, torch, pkg, knobs, name, grid):
+        """Golden frames with one env per CTA, and with at most 3 CTAs (every
+        CTA renders several envs: the cross-env prefetch of link trig and
+        distractor slot, the double-buffered link table, the video mbarrier
+        parity flip, the TMA store overlapping the next env)."""
+        if grid:
+            knobs.set("PXR_DEBUG_GRID", grid)
         rec = golden(f"render_{name}.npz")
         geom = geometry_of(name)
         poses = to_dev(torch, rec["poses"])
@@ -120,13 +120,13 @@ class TestRenderGolden:
         {"PXR_DEBUG_BAND_H": "7", "PXR_DEBUG_CAP": "40"},  # bands + rounds, plain stores
         {"PXR_DEBUG_NO_PACKED_SCAN": "1", "PXR_DEBUG_CAP": "40"},  # two-scan block scan
     ])
-    @pytest.mark.parametrize("variant", ["legacy", "pipe"])
-    def test_round_and_overflow_paths_exact(self, torch, pkg, knobs, kv, variant):
+    @pytest.mark.parametrize("grid", [0, 3])
+    def test_round_and_overflow_paths_exact(self, torch, pkg, knobs, kv, grid):
         """The multi-round and fragment-overflow paths (only reached by large
-        meshes / frames at default budgets) forced on the golden frames, for
-        both render kernels (the pipeline with several envs per CTA)."""
-        knobs.set("PXR_DEBUG_RENDER", variant)
-        knobs.set("PXR_DEBUG_GRID", 3)
+        meshes / frames at default budgets) forced on the golden frames; also
+        with at most 3 CTAs (several envs per CTA)."""
+        if grid:
+            knobs.set("PXR_DEBUG_GRID", grid)
         for k, v in kv.items():
             knobs.set(k, v)
         for name in ("humanoid_lite", "cheetah_lite"):
@@ -297,12 +297,11 @@ def fused_replay(torch, pkg, tag):
         np.testing.assert_array_equal(host["direction"], rec["final_direction"])
 
 
-@pytest.mark.parametrize("variant", ["auto", "legacy", "pipe"])
+@pytest.mark.parametrize("grid", [0, 3])
 @pytest.mark.parametrize("tag", REPLAYS)
-def test_fused_replay_hash_chain(torch, pkg, knobs, tag, variant):
-    if variant != "auto":
-        knobs.set("PXR_DEBUG_RENDER", variant)
-        knobs.set("PXR_DEBUG_GRID", 3)
+def test_fused_replay_hash_chain(torch, pkg, knobs, tag, grid):
+    if grid:  # several envs per CTA
+        knobs.set("PXR_DEBUG_GRID", grid)
     fused_replay(torch, pkg, tag)
 
 
