@@ -185,6 +185,10 @@ pxr_status pxr_div_check(const double *a, const double *b, double *q_pre, double
 /* Device sinf/cosf (glibc 2.39 restatement) for the parity test. */
 pxr_status pxr_sincosf(const float *x, float *s, float *c, int64_t n, void *stream);
 
+/* Device sin/cos in float64 (glibc 2.39 restatement, the physics' trig) for
+ * the parity test. */
+pxr_status pxr_sincos(const double *x, double *s, double *c, int64_t n, void *stream);
+
 /* Synthetic pose source for benchmarking: per env g =
  * env_offset + i, qpos = rest + U(-0.1, 0.1) from the reference reset keys
  * plus a deterministic joint oscillation at step t, then planar forward

@@ -37,6 +37,17 @@ _i8p = ctypes.POINTER(ctypes.c_int8)
 _I64 = ctypes.c_int64
 
 
+def sincos64(x):
+    """glibc 2.39 sin / cos in float64 (sin_glibc.c restatement), |x| < 105414350."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    s = np.empty_like(x)
+    c = np.empty_like(x)
+    dp = ctypes.POINTER(ctypes.c_double)
+    lib().glibc_sincos_batch(x.ctypes.data_as(dp), s.ctypes.data_as(dp), c.ctypes.data_as(dp),
+                             x.size)
+    return s, c
+
+
 def build() -> str:
     """Compile liboracle.so with the committed Makefile (idempotent)."""
     subprocess.run(["make", "-s", "-C", _HERE], check=True)
@@ -57,6 +68,8 @@ def lib():
         L.oracle_sincosf_selftest.argtypes = [ctypes.c_uint32] * 3
         L.oracle_sincosf_many.restype = None
         L.oracle_sincosf_many.argtypes = [_f32p, _f32p, _f32p, _I64]
+        L.glibc_sincos_batch.restype = None
+        L.glibc_sincos_batch.argtypes = [ctypes.POINTER(ctypes.c_double)] * 3 + [_I64]
         L.oracle_threefry2x64.restype = None
         L.oracle_threefry2x64.argtypes = [_u64p, _u64p, _I64, _u64p, _u64p, _u64p, _u64p, _I64]
         L.oracle_raster_scene.restype = None

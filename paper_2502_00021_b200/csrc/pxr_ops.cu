@@ -21,6 +21,7 @@
 
 #include "../../include/pxr.h"
 #include "pxr_internal.cuh"
+#include "pxr_glibc_sincos.cuh"
 #include "pxr_math.cuh"
 
 namespace pxr {
@@ -250,8 +251,8 @@ __global__ void sincosf_kernel(const float *x, float *s, float *c, int64_t n) {
   }
 }
 
-// physics.py:114-137, one thread per env, f64 (CUDA libdevice cos/sin: the
-// benchmark's pose source only needs the reference's value distribution).
+// physics.py:114-137, one thread per env, f64, with glibc's cos / sin
+// (pxr_glibc_sincos.cuh): bit-identical to the reference's numpy FK.
 __device__ __forceinline__ void fk_one(const double *q, const int32_t *parent,
                                        const double *adist, int nl, double *out) {
   out[0] = q[0];
@@ -260,8 +261,8 @@ __device__ __forceinline__ void fk_one(const double *q, const int32_t *parent,
   for (int i = 1; i < nl; i++) {
     const int pp = parent[i];
     const double th = out[3 * pp + 2];
-    out[3 * i + 0] = out[3 * pp + 0] + adist[i] * cos(th);
-    out[3 * i + 1] = out[3 * pp + 1] + adist[i] * sin(th);
+    out[3 * i + 0] = out[3 * pp + 0] + adist[i] * glibc_cos(th);
+    out[3 * i + 1] = out[3 * pp + 1] + adist[i] * glibc_sin(th);
     out[3 * i + 2] = th + q[3 + i - 1];
   }
 }
@@ -303,10 +304,10 @@ __global__ void pose_source_kernel(const double *rest, const int32_t *parent,
     const double time = 0.01 * (double)t;
     const double phase = (double)(g % 997) * 0.37;
     q[0] += time;                                  // root advances
-    q[1] += 0.03 * sin(6.0 * time + phase);        // bob
-    q[2] += 0.05 * sin(4.0 * time + phase);        // pitch rock
+    q[1] += 0.03 * glibc_sin(6.0 * time + phase);        // bob
+    q[2] += 0.05 * glibc_sin(4.0 * time + phase);        // pitch rock
     for (int j = 3; j < dof; j++)
-      q[j] += 0.6 * sin(8.0 * time + phase + 1.3 * j);
+      q[j] += 0.6 * glibc_sin(8.0 * time + phase + 1.3 * j);
     fk_one(q, parent, adist, nl, poses + b * nl * 3);
   }
 }
@@ -477,6 +478,23 @@ extern "C" pxr_status pxr_sincosf(const float *x, float *s, float *c, int64_t n,
   if (n == 0) return PXR_OK;
   sincosf_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, s, c, n);
   return check_launch("sincosf_kernel");
+}
+
+__global__ void sincos64_kernel(const double *x, double *s, double *c, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    s[i] = glibc_sin(v);
+    c[i] = glibc_cos(v);
+  }
+}
+
+extern "C" pxr_status pxr_sincos(const double *x, double *s, double *c, int64_t n, void *stream) {
+  if (n < 0 || (n > 0 && (x == nullptr || s == nullptr || c == nullptr)))
+    return set_invalid("bad sincos args");
+  if (n == 0) return PXR_OK;
+  sincos64_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, s, c, n);
+  return check_launch("sincos64_kernel");
 }
 
 extern "C" pxr_status pxr_forward_kinematics(const double *qpos, const int32_t *parent,

@@ -13,10 +13,14 @@
 //                     mass matrix, Cholesky, semi-implicit Euler, guard)
 //   compute_reward    physics.py:468-477
 //   reset_state / Env._reset_rows  physics.py:487-510, env.py:142-153
-// The only numerical difference from the reference is the f64 cos/sin/log
-// of CUDA's libdevice versus glibc/numpy (both faithfully rounded); every
-// other operation rounds identically (-fmad=false, same order). Physics is
-// OUTSIDE the bit-exact render contract: tests compare it with tolerances.
+// Every operation rounds as the reference's does (-fmad=false, same order)
+// and the f64 sin / cos are glibc's, restated (pxr_glibc_sincos.cuh), so
+// dynamics, rewards, FK and the reset qpos draws are bit-identical to the
+// reference (tests/test_env_gpu.py, test_physics_api.py; the recorded
+// reference rollouts reproduce in full, tests/test_recorder.py). The one
+// remaining difference is the log of the reset qvel Box-Muller draw
+// (prng.py:138-152): numpy evaluates it with its AVX-512 SVML log, the
+// device with CUDA's; they differ in the last bit on ~1 % of draws.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -24,6 +28,7 @@
 
 #include "../../include/pxr.h"
 #include "pxr_internal.cuh"
+#include "pxr_glibc_sincos.cuh"
 #include "pxr_math.cuh"
 
 namespace pxr {
@@ -196,8 +201,8 @@ __global__ void physics_step_kernel(StepArgs a) {
       theta[0] = qb[2];
       for (int i = 1; i < nl; i++) theta[i] = theta[m.parent[i]] + qb[3 + i - 1];
       for (int i = 0; i < nl; i++) {
-        ct[i] = cos(theta[i]);
-        st[i] = sin(theta[i]);
+        ct[i] = glibc_cos(theta[i]);
+        st[i] = glibc_sin(theta[i]);
       }
       omega[0] = qdb[2];
       ox[0] = qb[0]; oz[0] = qb[1];
@@ -361,8 +366,8 @@ __global__ void __launch_bounds__(kLanes == 8 ? 64 : 128) physics_step_warp_kern
       }
       __syncwarp();
       for (int i = lane; i < nl; i += kLanes) {
-        S.ct[i] = cos(S.theta[i]);
-        S.st[i] = sin(S.theta[i]);
+        S.ct[i] = glibc_cos(S.theta[i]);
+        S.st[i] = glibc_sin(S.theta[i]);
       }
       __syncwarp();
       if (lane == 0) {
@@ -553,8 +558,8 @@ __device__ void normal_draws(uint64_t khi, uint64_t klo, int n, double *out) {
     const double u2 = (double)(bits[mm + i] >> 11) * 0x1p-53;
     const double r = sqrt(-2.0 * log(u1));
     const double th = 2.0 * 3.141592653589793 * u2;
-    if (i < n) out[i] = r * cos(th);
-    if (mm + i < n) out[mm + i] = r * sin(th);
+    if (i < n) out[i] = r * glibc_cos(th);
+    if (mm + i < n) out[mm + i] = r * glibc_sin(th);
   }
 }
 
@@ -627,8 +632,8 @@ __global__ void fk_env_kernel(const double *qpos, const int32_t *parent, const d
     for (int i = 1; i < nl; i++) {
       const int pp = parent[i];
       const double th = out[3 * pp + 2];
-      out[3 * i + 0] = out[3 * pp + 0] + adist[i] * cos(th);
-      out[3 * i + 1] = out[3 * pp + 1] + adist[i] * sin(th);
+      out[3 * i + 0] = out[3 * pp + 0] + adist[i] * glibc_cos(th);
+      out[3 * i + 1] = out[3 * pp + 1] + adist[i] * glibc_sin(th);
       out[3 * i + 2] = th + q[3 + i - 1];
     }
   }

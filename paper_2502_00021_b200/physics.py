@@ -215,7 +215,10 @@ def compute_reward(spec: ModelSpec, prev: SystemState, next: SystemState, action
     p, q = _f64(prev.qpos, dev), _f64(next.qpos, dev)
     if a.shape[0] != p.shape[0] or p.shape[0] != q.shape[0]:
         raise ValueError("batch sizes disagree")
-    forward = (q[:, 0] - p[:, 0]) / spec.dt
+    # divide by a device tensor: ATen turns `tensor / python_float` into a
+    # multiply by the host-rounded reciprocal, which is not IEEE division
+    dt = torch.tensor(spec.dt, dtype=torch.float64, device=dev)
+    forward = (q[:, 0] - p[:, 0]) / dt
     ctrl = _np_row_sum(a * a) if a.shape[1] > 0 else torch.zeros_like(forward)
     return spec.forward_weight * forward - spec.ctrl_cost * ctrl
 

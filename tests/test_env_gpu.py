@@ -1,9 +1,12 @@
 """The reference's Env API (make_env / step / observe) on the device.
 
 Observations are bit-exact for a given state (the hot-path contract).
-Physics reproduces the reference's operation order but uses CUDA's f64
-cos/sin/log, so it is compared with tolerances;
-reset qpos draws (integer Threefry + f64 arithmetic) are bit-exact."""
+Physics reproduces the reference's operation order with glibc's f64 sin /
+cos restated on the device, so dynamics, rewards, FK and reset qpos draws
+are bit-exact. The reset qvel draws' Box-Muller log
+is numpy's AVX-512 SVML log on the reference host, not glibc's; CUDA's log
+differs from it in the last bit on ~1 % of draws, so qvel is compared to
+1e-13 relative."""
 
 import dataclasses
 import os
@@ -55,13 +58,12 @@ class TestPhysics:
             ctypes.byref(env.model_c), sys.qpos.data_ptr(), sys.qvel.data_ptr(),
             sys.step_count.data_ptr(), sys.done.data_ptr(), act.data_ptr(), reward.data_ptr(),
             32, _native.stream_ptr()))
-        np.testing.assert_allclose(sys.qpos.cpu().numpy(), rec[f"{name}_qpos1"], rtol=1e-9,
-                                   atol=1e-9)
-        np.testing.assert_allclose(sys.qvel.cpu().numpy(), rec[f"{name}_qvel1"], rtol=1e-8,
-                                   atol=1e-7)
+        # bit-exact: the reference's operation order, no FMA contraction, and
+        # glibc's sin / cos restated on the device (pxr_glibc_sincos.cuh)
+        np.testing.assert_array_equal(sys.qpos.cpu().numpy(), rec[f"{name}_qpos1"])
+        np.testing.assert_array_equal(sys.qvel.cpu().numpy(), rec[f"{name}_qvel1"])
         np.testing.assert_array_equal(sys.done.cpu().numpy().astype(bool), rec[f"{name}_done1"])
-        np.testing.assert_allclose(reward.cpu().numpy(), rec[f"{name}_reward"], rtol=1e-7,
-                                   atol=1e-6)
+        np.testing.assert_array_equal(reward.cpu().numpy(), rec[f"{name}_reward"])
 
     @pytest.mark.parametrize("name", MODEL_NAMES)
     def test_reset_draws(self, E, name):
@@ -105,8 +107,7 @@ def test_make_env_first_obs_matches_reference(E, tag, tmp_path):
                       observation=m["observation"], env_offset=m["env_offset"],
                       logical_batch=m["logical_batch"])
     env, state, obs = E.make_env(cfg)
-    np.testing.assert_allclose(env.poses(state.sys).cpu().numpy(), rec["poses"][0],
-                               rtol=0, atol=1e-12)
+    np.testing.assert_array_equal(env.poses(state.sys).cpu().numpy(), rec["poses"][0])
     np.testing.assert_array_equal(obs.cpu().numpy(), rec["first_obs"])
 
 

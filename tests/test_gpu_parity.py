@@ -48,6 +48,21 @@ class TestDeviceMath:
         assert np.array_equal(s.cpu().numpy().view(np.uint32), ws.view(np.uint32))
         assert np.array_equal(c.cpu().numpy().view(np.uint32), wc.view(np.uint32))
 
+    def test_sincos64_matches_libm(self, torch, pkg):
+        """Device glibc sin / cos in float64 (the physics' trig) against this
+        image's libm through numpy (physics.py:134-135, 529-538)."""
+        rng = np.random.default_rng(3)
+        x = np.concatenate([rng.uniform(-s, s, 1 << 20)
+                            for s in (1e-7, 0.126, 0.85, 2.43, 10.0, 300.0, 1e8)])
+        x = np.concatenate([x, np.linspace(-40.0, 40.0, 1 << 21)])
+        xd = to_dev(torch, x)
+        s = torch.empty_like(xd)
+        c = torch.empty_like(xd)
+        pkg._native.check(pkg._native.lib().pxr_sincos(
+            xd.data_ptr(), s.data_ptr(), c.data_ptr(), xd.numel(), pkg._native.stream_ptr()))
+        np.testing.assert_array_equal(s.cpu().numpy(), np.sin(x))
+        np.testing.assert_array_equal(c.cpu().numpy(), np.cos(x))
+
     def test_exact_division(self, torch, pkg):
         """The raster's division (per-triangle RN reciprocal + one Markstein
         correction) must equal IEEE a / b for every operand it can see."""

@@ -60,6 +60,30 @@ class TestOracleSinCosf:
         assert bad == 0 and lo > 0
 
 
+class TestOracleSinCos64:
+    """oracle/sin_glibc.c (glibc 2.39 sin / cos restated with the -mfma
+    build's contractions as explicit fma) against this image's libm, which
+    numpy's float64 np.sin / np.cos call (physics.py:134-135, 529-538)."""
+
+    def test_matches_libm(self, oracle):
+        rng = np.random.default_rng(7)
+        for scale in (1e-7, 0.126, 0.85, 2.43, 10.0, 1e3, 1e8):
+            x = rng.uniform(-scale, scale, 400_000)
+            s, c = oracle.sincos64(x)
+            np.testing.assert_array_equal(s, np.sin(x))
+            np.testing.assert_array_equal(c, np.cos(x))
+
+    def test_range_edges(self, oracle):
+        edges = np.array([0x3e400000, 0x3e500000, 0x3feb6000, 0x400368fd, 0x419921fa],
+                         dtype=np.uint64) << np.uint64(32)
+        x = np.concatenate([(edges + np.uint64(d)).view(np.float64) for d in (0, 1, 2)] +
+                           [(edges - np.uint64(d)).view(np.float64) for d in (1, 2)])
+        x = np.concatenate([x, -x, [0.0, -0.0, 0.126, -0.126, np.pi / 2, np.pi]])
+        s, c = oracle.sincos64(x)
+        np.testing.assert_array_equal(s, np.sin(x))
+        np.testing.assert_array_equal(c, np.cos(x))
+
+
 class TestOracleRender:
     @pytest.mark.parametrize("name", MODEL_NAMES)
     def test_matches_reference_frames(self, oracle, name):

@@ -52,13 +52,11 @@ class TestPhysicsAPI:
         act = rec[f"{name}_act"]
         nxt = pkg.step_dynamics(spec, st, act)
         assert nxt is not st and torch.equal(st.qpos, torch.from_numpy(rec[f"{name}_qpos"]).cuda())
-        np.testing.assert_allclose(nxt.qpos.cpu().numpy(), rec[f"{name}_qpos1"], rtol=1e-9,
-                                   atol=1e-9)
-        np.testing.assert_allclose(nxt.qvel.cpu().numpy(), rec[f"{name}_qvel1"], rtol=1e-8,
-                                   atol=1e-7)
+        np.testing.assert_array_equal(nxt.qpos.cpu().numpy(), rec[f"{name}_qpos1"])
+        np.testing.assert_array_equal(nxt.qvel.cpu().numpy(), rec[f"{name}_qvel1"])
         np.testing.assert_array_equal(nxt.done.cpu().numpy().astype(bool), rec[f"{name}_done1"])
         r = pkg.compute_reward(spec, st, nxt, act)
-        np.testing.assert_allclose(r.cpu().numpy(), rec[f"{name}_reward"], rtol=1e-7, atol=1e-6)
+        np.testing.assert_array_equal(r.cpu().numpy(), rec[f"{name}_reward"])
         term = pkg.check_termination(spec, nxt).cpu().numpy()
         if spec.min_root_height is None:
             assert not term.any()
@@ -115,7 +113,7 @@ class TestPhysicsAPI:
         spec = spec_of("humanoid_lite")
         q = np.random.default_rng(1).uniform(-1, 1, (9, spec.dof))
         got = pkg.forward_kinematics(spec, q).cpu().numpy()
-        np.testing.assert_allclose(got, forward_kinematics_host(spec, q), rtol=0, atol=1e-12)
+        np.testing.assert_array_equal(got, forward_kinematics_host(spec, q))
 
     def test_ballistic_within_1e_3(self, pkg, torch):
         from paper_2502_00021_b200.models import LinkSpec, ModelSpec

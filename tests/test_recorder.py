@@ -126,19 +126,18 @@ class TestRecorderGPU:
         with pytest.raises(ValueError):
             R.record_rollout(cfg, "zeros", 0)
 
-    # Minimum matching prefix per recorded chain (measured on B200: the four
-    # shorter chains match in full, BASELINE config 1 up to t = 281 of 1000).
-    PREFIX = {"cheetah_none_b1": 250, "walker_video_b8": None, "ant_color_b8": None,
+    # Every recorded chain is reproduced in full, BASELINE config 1's
+    # 1000 steps included (None = no divergence allowed).
+    PREFIX = {"cheetah_none_b1": None, "walker_video_b8": None, "ant_color_b8": None,
               "humanoid_video_b8_slice": None, "hopper_color_gray_b4": None}
 
     @pytest.mark.parametrize("tag", list(PREFIX))
     def test_reference_chain_prefix(self, R, tag, tmp_path):
         """The reference recorded these chains with record_rollout's
-        ``random:<seed>`` policy. Reset draws, policy keys, distractors and
-        the render are bit-exact; the dynamics use CUDA's f64 cos/sin/log (not
-        numpy's), so a chain may part once a physics rounding difference
-        reaches a pixel: full-chain equality where it was measured, else the
-        measured prefix."""
+        ``random:<seed>`` policy. Policy keys, distractors, the render and the
+        dynamics are bit-exact (glibc sin / cos on the device); a reset's
+        qvel draw could differ in the last bit (numpy's SVML log), which
+        none of these chains hits."""
         import paper_2502_00021_b200 as P
 
         E = self._env_mod()
