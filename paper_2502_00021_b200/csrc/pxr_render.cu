@@ -80,6 +80,9 @@ constexpr uint32_t kDecBit = 0x80000000u;
 // live triangles that cover no pixel centre, their bbox-row units, those of
 // them with a single bbox row
 constexpr int kStats = 10;
+// debug phase timer slots (p.prof, tools/phase_prof.py): thread 0's clock at
+// each phase-ending barrier, accumulated per CTA
+constexpr int kProfSlots = 12;
 #ifdef PXR_CHECKED
 constexpr bool kWithStats = true;  // counters only in the checked build
 #else
@@ -161,6 +164,11 @@ struct RenderParams {
   int band_h;       // rows per band: a frame is rendered in bands that fit shared memory
   int32_t *stats;   // debug (tools/render_stats.py): per env kStats workload counters, or null
   int scan_sh;      // > 0: live count << scan_sh | bbox rows fits 32 bits (one packed scan)
+  long long *prof;  // debug (tools/phase_prof.py): per-CTA phase cycles, or null
+  // Small batches: `split` CTAs (one thread-block cluster) render one env,
+  // one row band each; 1 = persistent CTAs, each a sequence of whole envs.
+  int split;
+  int64_t env_stride;  // envs between a CTA's consecutive envs (= gridDim.x / split)
 };
 
 struct SmemLayout {
@@ -217,6 +225,8 @@ struct EnvShared {
   int one_round;  // all live triangles of the band fit one raster round
   int plan_ok;
   int st[kStats];  // debug counters (p.stats)
+  long long prof[kProfSlots];  // debug phase cycles (p.prof)
+  long long prof_t;
 };
 
 // Per-env distractor step (writes the new state back to HBM):
@@ -225,8 +235,10 @@ struct EnvShared {
 //   video:  ping-pong cursor (distractor.py:128-136), then for envs being
 //           reset the re-drawn video (env.py:226-244); frame index 204.
 // With advance == 0 (make_env / observe) the stored state is used as is.
+// write == false: compute only (the bands of a split env all compute the
+// step; one writes it back once the cluster has read the old state).
 __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t env,
-                                                  DistSlot &out) {
+                                                  DistSlot &out, bool write = true) {
   const uint64_t g = p.env_offset + (uint64_t)env;
   out.bias[0] = out.bias[1] = out.bias[2] = 0;
   out.frame_idx = 0;
@@ -238,7 +250,8 @@ __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t
       uint64_t ehi, elo;
       threefry2x64(key_hi, key_lo, g, 2, ehi, elo);
       color_bias_from_key(ehi, elo, b3);
-      for (int c = 0; c < 3; c++) p.color_bias[env * 3 + c] = b3[c];
+      if (write)
+        for (int c = 0; c < 3; c++) p.color_bias[env * 3 + c] = b3[c];
     } else {
       for (int c = 0; c < 3; c++) b3[c] = p.color_bias[env * 3 + c];
     }
@@ -261,11 +274,15 @@ __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t
         vid = index_from_word(w0, (uint64_t)p.n_videos);
         cur = 0;
         dir = 1;
-        p.video_index[env] = vid;
-        p.frame_count[env] = p.counts[vid];
+        if (write) {
+          p.video_index[env] = vid;
+          p.frame_count[env] = p.counts[vid];
+        }
       }
-      p.frame_cursor[env] = cur;
-      p.direction[env] = (int8_t)dir;
+      if (write) {
+        p.frame_cursor[env] = cur;
+        p.direction[env] = (int8_t)dir;
+      }
     }
     PXR_DCHECK(vid >= 0 && vid < p.n_videos);
     PXR_DCHECK(cur >= 0 && cur < p.counts[vid]);
@@ -339,7 +356,7 @@ __device__ __forceinline__ void pixel_range(float mn, float mx, int lim, int &lo
 // envs of this CTA is advanced at once, one lane each.
 __device__ __forceinline__ void prepare_env(const RenderParams &p, int64_t env, int local_env,
                                          float4 *link_buf, DistSlot *s_dist, EnvShared &es,
-                                         int lane) {
+                                         int lane, bool write = true) {
   for (int l = lane; l < p.nl; l += 32) {
     const double *pp = p.poses + (env * p.nl + l) * 3;
     const float th = (float)pp[2];  // poses.astype(float32), render.py:613
@@ -347,8 +364,8 @@ __device__ __forceinline__ void prepare_env(const RenderParams &p, int64_t env, 
                               glibc_sincosf(th, 0));
   }
   if (local_env % 32 == 0) {
-    const int64_t e2 = env + (int64_t)lane * gridDim.x;
-    if (e2 < p.batch) distractor_update(p, e2, s_dist[lane]);
+    const int64_t e2 = env + (int64_t)lane * p.env_stride;
+    if (e2 < p.batch) distractor_update(p, e2, s_dist[lane], write);
   }
   __syncwarp();
   if (lane == 0) {
@@ -490,6 +507,16 @@ __device__ __forceinline__ void put_rgb(uint8_t *col, uint32_t pix, uint32_t rgb
   col[3 * pix + 2] = (uint8_t)(rgb >> 16);
 }
 
+// Phase timer (debug): thread 0 adds the cycles since its last mark to a slot.
+#define PXR_PROF(slot)                                  \
+  do {                                                  \
+    if (p.prof != nullptr && tid == 0) {                \
+      const long long now_ = clock64();                 \
+      es.prof[slot] += now_ - es.prof_t;                \
+      es.prof_t = now_;                                 \
+    }                                                   \
+  } while (0)
+
 // kBands = false: the whole frame is one band (y0 = 0, straight-line code).
 // kFloor = draw_floor: the checker floor needs every thread for the
 // background (f64 per pixel), without it the background is cheap enough for
@@ -571,6 +598,8 @@ render_step_kernel(const RenderParams p) {
     mbar_init(&es.vbar, 1);
     fence_mbar_init();
     es.plan_ok = 0;
+    for (int i = 0; i < kProfSlots; i++) es.prof[i] = 0;
+    es.prof_t = p.prof != nullptr ? clock64() : 0;
   }
   __syncthreads();
   // Byte-permute plan of the NN video gather (distractor.py:172-176): with
@@ -613,9 +642,22 @@ render_step_kernel(const RenderParams p) {
   __syncthreads();
   const bool plan_ok = use_plan && es.plan_ok == 0;
 
-  if (warp == kWarps - 1 && blockIdx.x < p.batch)
-    prepare_env(p, blockIdx.x, 0, s_link, s_dist, es, lane);
+  // split env: this CTA renders band `band0` of env blockIdx.x / split
+  const int band0 = p.split > 1 ? (int)(blockIdx.x % (unsigned)p.split) : 0;
+  const int64_t env_first = p.split > 1 ? (int64_t)(blockIdx.x / (unsigned)p.split) : blockIdx.x;
+  if (warp == kWarps - 1 && env_first < p.batch)
+    prepare_env(p, env_first, 0, s_link, s_dist, es, lane, p.split == 1);
   __syncthreads();
+  if (p.split > 1) {
+    // every band has read the env's distractor state: band 0 writes its step
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (band0 == 0 && p.advance && warp == kWarps - 1 && lane == 0) {
+      DistSlot unused;
+      distractor_update(p, env_first, unused, true);
+    }
+  }
+  PXR_PROF(0);  // once per CTA: setup + the first env's preparation
 
   // liveness: each thread owns a contiguous block of triangles (index order)
   const int per = (p.nt + kThreads - 1) / kThreads;
@@ -633,34 +675,14 @@ render_step_kernel(const RenderParams p) {
     g_bz = __ldg(p.base_verts + 3 * tid + 2);
   }
 
-  uint32_t vphase = 0;
-  int local_env = 0;
-  for (int64_t env = blockIdx.x; env < p.batch; env += gridDim.x, local_env++) {
-    // ---- phase 0: video fetch (the env's link trig, camera and distractor
-    // state were prepared by warp kWarps-1 during the previous env) -------
-    const int cb = local_env & 1;
-    const float4 *s_link_cur = s_link + cb * p.nl;
-    if (kWithStats && p.stats != nullptr && tid < kStats) es.st[tid] = 0;
-    if (tid == 0 && p.mode == PXR_MODE_VIDEO && p.vframe_bulk) {
-      PXR_DCHECK(es.frame_idx[cb] >= 0 && es.frame_idx[cb] < p.n_frames);
-      mbar_arrive_expect_tx(&es.vbar, (uint32_t)p.vframe_bytes);
-      bulk_load_g2s(s_vframe, p.frames + es.frame_idx[cb] * p.vframe_bytes,
-                    (uint32_t)p.vframe_bytes, &es.vbar);
-    }
-    const float ex = es.ex[cb], ez = es.ez[cb];
-    bool prepared = env + gridDim.x >= p.batch;  // nothing to prepare for a last env
-
-    // the first liveness triangle's indices, loaded before the vertex phase
-    // so their latency (L2: the geometry does not stay in the small L1 next
-    // to 230 KB of shared memory) overlaps it
-    int n0 = 0, n1 = 0, n2 = 0;  // indices of the next triangle, loaded one ahead
-    if (t0 < t1) {
-      n0 = __ldg(p.tris + 3 * t0 + 0);
-      n1 = __ldg(p.tris + 3 * t0 + 1);
-      n2 = __ldg(p.tris + 3 * t0 + 2);
-    }
-
-    // ---- phase 1: world transform + projection (render.py:468-481, 350-363)
+  // Phase 1 of local env lenv (render.py:468-481, 350-363): world transform +
+  // projection of every vertex, and with a separable floor its per-row terms
+  // (t = -ez / dz, parity of floor(wy); render.py:321-334) by the last
+  // threads (those with no or one vertex). Reads the env's prepared link
+  // trig / camera (parity lenv & 1).
+  auto vertex_phase = [&](int lenv) {
+    const float4 *s_lk = s_link + (lenv & 1) * p.nl;
+    const float lex = es.ex[lenv & 1], lez = es.ez[lenv & 1];
     if (kFloor && p.floor_sep) {
       // separable floor rays: t = -ez / dz and floor(wy) depend on the row
       // only (render.py:321-334), computed once per row by the last threads
@@ -670,7 +692,7 @@ render_step_kernel(const RenderParams p) {
         double t = 0.0;
         int k = -1;  // -1: sky; else parity of floor(wy)
         if (dz < -1e-12) {
-          t = (double)(-ez) / dz;
+          t = (double)(-lez) / dz;
           if ((double)p.cam[13] <= t && t <= (double)p.cam[14]) {
             const double wy = (double)p.cam[1] + t * dy;
             k = (int)(__double2ll_rd(wy) & 1);
@@ -683,15 +705,15 @@ render_step_kernel(const RenderParams p) {
     for (int v = tid; v < p.nv; v += kThreads) {
       float3 w;
       if (v == tid) {  // the thread's first vertex: geometry held in registers
-        const float4 lk = s_link_cur[g_link];
+        const float4 lk = s_lk[g_link];
         w = make_float3(lk.x + g_bx * lk.z - g_bz * lk.w, g_by, lk.y + g_bx * lk.w + g_bz * lk.z);
       } else {
-        w = world_vertex(p, s_link_cur, v);
+        w = world_vertex(p, s_lk, v);
       }
       s_world[3 * v + 0] = w.x;
       s_world[3 * v + 1] = w.y;
       s_world[3 * v + 2] = w.z;
-      const float vx = w.x - ex, vy = w.y - ey, vz = w.z - ez;
+      const float vx = w.x - lex, vy = w.y - ey, vz = w.z - lez;
       const float zv = vx * fx + vy * fy + vz * fz;
       float sx = 0.0f, sy = 0.0f;
       if ((double)zv > 1e-9) {
@@ -706,14 +728,46 @@ render_step_kernel(const RenderParams p) {
       s_vxy64[v] = make_double2((double)sx, (double)sy);
       s_viz[v] = __drcp_rn((double)zv);  // iz = 1.0 / z (render.py:434-436)
     }
+  };
+
+  uint32_t vphase = 0;
+  int local_env = 0;
+  for (int64_t env = env_first; env < p.batch; env += p.env_stride, local_env++) {
+    // ---- phase 0: video fetch (the env's link trig, camera and distractor
+    // state were prepared by warp kWarps-1 during the previous env) -------
+    const int cb = local_env & 1;
+    if (kWithStats && p.stats != nullptr && tid < kStats) es.st[tid] = 0;
+    if (tid == 0 && p.mode == PXR_MODE_VIDEO && p.vframe_bulk) {
+      PXR_DCHECK(es.frame_idx[cb] >= 0 && es.frame_idx[cb] < p.n_frames);
+      mbar_arrive_expect_tx(&es.vbar, (uint32_t)p.vframe_bytes);
+      bulk_load_g2s(s_vframe, p.frames + es.frame_idx[cb] * p.vframe_bytes,
+                    (uint32_t)p.vframe_bytes, &es.vbar);
+    }
+    const float ex = es.ex[cb], ez = es.ez[cb];
+    bool prepared = env + p.env_stride >= p.batch;  // nothing to prepare for a last env
+
+    // the first liveness triangle's indices, loaded before the vertex phase
+    // so their latency (L2: the geometry does not stay in the small L1 next
+    // to 230 KB of shared memory) overlaps it
+    int n0 = 0, n1 = 0, n2 = 0;  // indices of the next triangle, loaded one ahead
+    if (t0 < t1) {
+      n0 = __ldg(p.tris + 3 * t0 + 0);
+      n1 = __ldg(p.tris + 3 * t0 + 1);
+      n2 = __ldg(p.tris + 3 * t0 + 2);
+    }
+
+    // ---- phase 1: world transform + projection (render.py:468-481, 350-363)
+    vertex_phase(local_env);
     // The previous env's TMA store must have finished reading the frame.
     if (tid == 0 && p.use_bulk) bulk_wait_read();
     __syncthreads();
+    PXR_PROF(1);  // vertex transform + projection
 
     // ---- bands of rows: everything below runs once per band (one band
     // whenever the frame's per-pixel state fits shared memory) ------------
     const int band_h = kBands ? p.band_h : p.H;
-    int yb = 0;
+    const int ystart = kBands ? band0 * band_h : 0;  // a split env: this CTA's band only
+    int yb = ystart;
     do {  // (no loop at all for one band)
       const int y0 = kBands ? yb : 0;  // compile-time 0 for one band
       const int y1 = kBands ? min(y0 + band_h, p.H) : p.H;
@@ -742,7 +796,7 @@ render_step_kernel(const RenderParams p) {
         else
           put_rgb(s_col, pix, rgb);
       };
-      if (kBands && y0 > 0) {  // the previous band's TMA store must have finished reading
+      if (kBands && y0 > ystart) {  // the previous band's TMA store must have finished reading
         if (tid == 0 && p.use_bulk) bulk_wait_read();
         __syncthreads();
       }
@@ -751,7 +805,7 @@ render_step_kernel(const RenderParams p) {
       // each thread's block of triangles (t0, t1) is contiguous, so its live
       // count and bbox-row total feed the block scan directly
       int my_live = 0, my_rows = 0;
-      if (kBands && y0 > 0 && t0 < t1) {  // (the first band's were loaded at the env's start)
+      if (kBands && y0 > ystart && t0 < t1) {  // (the first band's were loaded at the env's start)
         n0 = __ldg(p.tris + 3 * t0 + 0);
         n1 = __ldg(p.tris + 3 * t0 + 1);
         n2 = __ldg(p.tris + 3 * t0 + 2);
@@ -796,9 +850,9 @@ render_step_kernel(const RenderParams p) {
       // a floor (cheap texel / sky pixels) it is written by the warps the
       // records phase leaves idle (see below), else here by every thread:
       // threads first, first + stride, ...
-      const bool vwait = y0 == 0 && p.mode == PXR_MODE_VIDEO && p.vframe_bulk;
+      const bool vwait = y0 == ystart && p.mode == PXR_MODE_VIDEO && p.vframe_bulk;
       const uint32_t vpar = vphase;
-      if (y0 == 0) vphase ^= 1u;  // the env's video frame (one fetch for all bands)
+      if (y0 == ystart) vphase ^= 1u;  // the env's video frame (one fetch for all bands)
       auto background = [&](int first, int stride) {
         if (vwait) mbar_wait_parity(&es.vbar, vpar);
         if (p.mode == PXR_MODE_VIDEO && !kFloor && plan_ok && !p.gray) {
@@ -959,6 +1013,7 @@ render_step_kernel(const RenderParams p) {
         }
       }
       __syncthreads();
+      PXR_PROF(2);  // liveness + block scan (+ floor background)
       const int n_live = es.n_live;
       const bool one_round = es.one_round != 0;
       if (!kFloor && n_live == 0) {
@@ -1080,6 +1135,7 @@ render_step_kernel(const RenderParams p) {
           background(bg_split ? tid - rec_warps * 32 : tid,
                      bg_split ? kThreads - rec_warps * 32 : kThreads);
         __syncthreads();
+        PXR_PROF(3);  // records + span equations (+ video / sky background)
 
         // (triangle, bbox row) units, 32 per chunk, chunks dealt round-robin
         // to the warps: each lane computes one row's conservative span and the
@@ -1092,7 +1148,7 @@ render_step_kernel(const RenderParams p) {
         // the other warps only (it would otherwise finish last)
         const int n_workers = prepared ? kWarps : kWarps - 1;
         if (warp == kWarps - 1 && !prepared) {
-          prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
+          prepare_env(p, env + p.env_stride, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
                       lane);
           prepared = true;
         }
@@ -1207,6 +1263,7 @@ render_step_kernel(const RenderParams p) {
           }
         }
         __syncthreads();
+        PXR_PROF(4);  // row spans -> candidates -> exact test -> fragments
 
         // exact sequential-order resolve (see the file header)
         const int n_frag = es.n_frag;
@@ -1241,6 +1298,7 @@ render_step_kernel(const RenderParams p) {
             }
           }
           __syncthreads();
+          PXR_PROF(5);  // resolve pass
           for (int i = tid; i < n_frag; i += kThreads) {
             const uint32_t pix = s_frag[i].y & 0xFFFFFu, tri = s_frag[i].y >> 20;
             if (resolve_winner(s_wkey[pix]) == (int)tri) emit(pix, s_rec[tri].rgb);
@@ -1288,7 +1346,7 @@ render_step_kernel(const RenderParams p) {
         r0 = r1;
       }
       if (warp == kWarps - 1 && !prepared)  // env without live triangles
-        prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es, lane);
+        prepare_env(p, env + p.env_stride, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es, lane);
 
       // ---- depth output (debug / _render_frame parity only) ---------------
       if (p.out_depth != nullptr) {
@@ -1308,6 +1366,7 @@ render_step_kernel(const RenderParams p) {
       if (p.use_bulk) {  // host: every band's size and offset are multiples of 16
         fence_proxy_async_smem();
         __syncthreads();
+        PXR_PROF(6);  // paint (+ depth output)
         if (tid == 0) bulk_store_s2g(gout, s_out, (uint32_t)band_bytes);
       } else {
         __syncthreads();
@@ -1315,9 +1374,15 @@ render_step_kernel(const RenderParams p) {
         __syncthreads();
       }
       yb += band_h;
-    } while (kBands && yb < p.H);
+    } while (kBands && p.split == 1 && yb < p.H);
   }
   if (tid == 0 && p.use_bulk) bulk_wait_all();
+  if (p.prof != nullptr) {
+    PXR_PROF(7);  // the last store's completion
+    if (tid == 0) es.prof[8] = local_env;
+    __syncthreads();
+    if (tid < kProfSlots) p.prof[blockIdx.x * kProfSlots + tid] = es.prof[tid];
+  }
 }
 
 // One thread per image row walks x exactly like render.py:321-344.
@@ -1500,6 +1565,9 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   // per CTA (the cross-env prefetch, double-buffered link table, video
   // mbarrier parity flip and TMA-store overlap)
   const int64_t debug_grid = debug_int(kDbgGrid, 0);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // debug: a device int64 (grid, 12) buffer for per-CTA phase cycles
+  p.prof = (long long *)(uintptr_t)debug_int(kDbgProf, 0);
 
   const DeviceFacts &dev = device_facts();
   const int max_optin = dev.max_smem_optin;
@@ -1526,6 +1594,26 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
       if (smem_layout(p).total <= budget) break;
     }
     if (debug_band > 0 && debug_band < bh) bh = debug_band;
+    // Small batches (at least two SMs per env): each env is split over a
+    // thread-block cluster of up to 8 CTAs, one row band each, so the
+    // latency-bound single-env chain runs on several SMs (the raster and
+    // background work divide by the band count; vertices and liveness are
+    // recomputed per band).
+    p.split = 1;
+    const int64_t dsplit = debug_int(kDbgSplit, -1);  // 0: never; n > 0: force n bands
+    if (dsplit != 0 && bh == height && p.stats == nullptr && debug_grid == 0) {
+      int64_t want = dsplit > 0 ? dsplit : (batch * 2 <= dev.num_sms ? dev.num_sms / batch : 1);
+      if (want > 8) want = 8;
+      if (want > 1) {
+        int sb = (int)((height + want - 1) / want);
+        if (sb % m) sb += m - sb % m;
+        const int nb = (height + sb - 1) / sb;
+        if (nb >= 2) {
+          p.split = nb;
+          bh = sb;
+        }
+      }
+    }
     p.band_h = bh;
     if (bh < height && (bh * bytes_row) % 16 != 0) p.use_bulk = 0;
     if (bh < height && (bh * width) % 4 != 0) p.depth_vec = 0;
@@ -1554,7 +1642,25 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   int64_t grid = (int64_t)dev.num_sms * per_sm;
   if (debug_grid > 0 && debug_grid < grid) grid = debug_grid;
   if (grid > batch) grid = batch;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (p.split > 1) {  // one cluster of `split` CTAs per env
+    p.env_stride = batch;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(batch * p.split));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)p.split;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, p);
+    if (e != cudaSuccess) return set_cuda(e, "render_step_kernel (cluster launch)");
+    return check_launch("render_step_kernel");
+  }
+  p.env_stride = grid;
   kernel<<<(unsigned)grid, kThreads, smem, st>>>(p);
   return check_launch("render_step_kernel");
 }
