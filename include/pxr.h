@@ -111,7 +111,7 @@ const char *pxr_status_string(pxr_status s);
 const char *pxr_last_error(void);
 /* Test / debug knobs (no reference counterpart): `name` is one of
  * PXR_DEBUG_FRAG_LIMIT, _ROW_CAP, _CAP, _STATS_PTR, _BAND_H, _NO_PACKED_SCAN,
- * _PHYS, _GRID, _PROF, _SPLIT; `value` its string value, NULL to unset. The PXR_DEBUG_*
+ * _PHYS, _GRID, _PROF; `value` its string value, NULL to unset. The PXR_DEBUG_*
  * environment is read once at the first query; this overrides it. */
 pxr_status pxr_set_debug(const char *name, const char *value);
 

@@ -60,6 +60,7 @@ class Workload:
         self.floor_in_background = mode == "video"  # env.py:81-85 default
         self.width, self.height = int(width), int(height)
         self.master = key_from_seed(seed)
+        self._keys: dict = {}
         self.reset_key = fold_in(self.master, 0x5EED)
         self.renderer = RobotRenderer(self.geom, CameraConfig(), width, height, self.device)
         self.pack = None
@@ -101,11 +102,25 @@ class Workload:
             self.batch, out.data_ptr(), _native.stream_ptr(stream)))
         return out
 
+    def step_keys(self, t: int):
+        """The launch's step keys (key_t = fold_in(master, t), env.py:209),
+        memoised: the host Threefry costs ~18 us in Python, more than a
+        small batch's whole render, so timed loops precompute them."""
+        k = self._keys.get(t)
+        if k is None:
+            k = step_keys(fold_in(self.master, t), self.env_offset, self.logical_batch)
+            self._keys[t] = k
+        return k
+
+    def precompute_keys(self, ts) -> None:
+        for t in ts:
+            self.step_keys(t)
+
     def render(self, poses, t: int, advance: bool = True, want_depth: bool = False,
                out_obs=None, stream=None, done=None):
         """The rendered env-step proper: key_t = fold_in(master, t), advance
         distractors, render, composite, postprocess -- one launch."""
-        keys = step_keys(fold_in(self.master, t), self.env_offset, self.logical_batch)
+        keys = self.step_keys(t)
         return self.renderer.render(
             poses, floor_in_background=self.floor_in_background, dist=self.dist,
             pack=self.dpack, advance=advance, keys=keys, done=done, grayscale=self.grayscale,

@@ -55,7 +55,6 @@ enum DebugKnob {
   kDbgPhys,          // PXR_DEBUG_PHYS: warp|half|quarter|thread physics kernel
   kDbgGrid,          // PXR_DEBUG_GRID: at most this many CTAs (several envs per CTA)
   kDbgProf,          // PXR_DEBUG_PROF: device int64 (grid, 12) per-CTA phase cycles
-  kDbgSplit,         // PXR_DEBUG_SPLIT: 0 = never split an env over CTAs, n = n bands
   kDbgCount
 };
 // value of a knob, or nullptr when unset

@@ -165,10 +165,6 @@ struct RenderParams {
   int32_t *stats;   // debug (tools/render_stats.py): per env kStats workload counters, or null
   int scan_sh;      // > 0: live count << scan_sh | bbox rows fits 32 bits (one packed scan)
   long long *prof;  // debug (tools/phase_prof.py): per-CTA phase cycles, or null
-  // Small batches: `split` CTAs (one thread-block cluster) render one env,
-  // one row band each; 1 = persistent CTAs, each a sequence of whole envs.
-  int split;
-  int64_t env_stride;  // envs between a CTA's consecutive envs (= gridDim.x / split)
 };
 
 struct SmemLayout {
@@ -235,10 +231,8 @@ struct EnvShared {
 //   video:  ping-pong cursor (distractor.py:128-136), then for envs being
 //           reset the re-drawn video (env.py:226-244); frame index 204.
 // With advance == 0 (make_env / observe) the stored state is used as is.
-// write == false: compute only (the bands of a split env all compute the
-// step; one writes it back once the cluster has read the old state).
 __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t env,
-                                                  DistSlot &out, bool write = true) {
+                                                  DistSlot &out) {
   const uint64_t g = p.env_offset + (uint64_t)env;
   out.bias[0] = out.bias[1] = out.bias[2] = 0;
   out.frame_idx = 0;
@@ -250,8 +244,7 @@ __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t
       uint64_t ehi, elo;
       threefry2x64(key_hi, key_lo, g, 2, ehi, elo);
       color_bias_from_key(ehi, elo, b3);
-      if (write)
-        for (int c = 0; c < 3; c++) p.color_bias[env * 3 + c] = b3[c];
+      for (int c = 0; c < 3; c++) p.color_bias[env * 3 + c] = b3[c];
     } else {
       for (int c = 0; c < 3; c++) b3[c] = p.color_bias[env * 3 + c];
     }
@@ -274,15 +267,11 @@ __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t
         vid = index_from_word(w0, (uint64_t)p.n_videos);
         cur = 0;
         dir = 1;
-        if (write) {
-          p.video_index[env] = vid;
-          p.frame_count[env] = p.counts[vid];
-        }
+        p.video_index[env] = vid;
+        p.frame_count[env] = p.counts[vid];
       }
-      if (write) {
-        p.frame_cursor[env] = cur;
-        p.direction[env] = (int8_t)dir;
-      }
+      p.frame_cursor[env] = cur;
+      p.direction[env] = (int8_t)dir;
     }
     PXR_DCHECK(vid >= 0 && vid < p.n_videos);
     PXR_DCHECK(cur >= 0 && cur < p.counts[vid]);
@@ -356,7 +345,7 @@ __device__ __forceinline__ void pixel_range(float mn, float mx, int lim, int &lo
 // envs of this CTA is advanced at once, one lane each.
 __device__ __forceinline__ void prepare_env(const RenderParams &p, int64_t env, int local_env,
                                          float4 *link_buf, DistSlot *s_dist, EnvShared &es,
-                                         int lane, bool write = true) {
+                                         int lane) {
   for (int l = lane; l < p.nl; l += 32) {
     const double *pp = p.poses + (env * p.nl + l) * 3;
     const float th = (float)pp[2];  // poses.astype(float32), render.py:613
@@ -364,8 +353,8 @@ __device__ __forceinline__ void prepare_env(const RenderParams &p, int64_t env, 
                               glibc_sincosf(th, 0));
   }
   if (local_env % 32 == 0) {
-    const int64_t e2 = env + (int64_t)lane * p.env_stride;
-    if (e2 < p.batch) distractor_update(p, e2, s_dist[lane], write);
+    const int64_t e2 = env + (int64_t)lane * gridDim.x;
+    if (e2 < p.batch) distractor_update(p, e2, s_dist[lane]);
   }
   __syncwarp();
   if (lane == 0) {
@@ -580,18 +569,23 @@ render_step_kernel(const RenderParams p) {
   const uint32_t lanemask_lt = (1u << lane) - 1u;
   const uint32_t lanemask_le = 0xFFFFFFFFu >> (31 - lane);
 
-  // ---- once per CTA: floor rays, NN maps, mbarrier -----------------------
-  if (kFloor && p.floor_sep) {
-    for (int i = tid; i < p.W; i += kThreads) s_floor[i] = p.floor_rays[(int64_t)i * 3];
-    for (int i = tid; i < p.H; i += kThreads) {
+  // ---- once per CTA: floor rays, NN maps, mbarrier; meanwhile the last
+  // warp prepares the first env (its latency chain would otherwise open the
+  // CTA's critical path: a whole launch at small batches) ------------------
+  constexpr int kSetupThreads = kThreads - 32;  // every warp but the last
+  if (warp == kWarps - 1 && blockIdx.x < p.batch)
+    prepare_env(p, blockIdx.x, 0, s_link, s_dist, es, lane);
+  if (kFloor && p.floor_sep && warp < kWarps - 1) {
+    for (int i = tid; i < p.W; i += kSetupThreads) s_floor[i] = p.floor_rays[(int64_t)i * 3];
+    for (int i = tid; i < p.H; i += kSetupThreads) {
       s_floor[p.W + i] = p.floor_rays[(int64_t)i * p.W * 3 + 1];
       s_floor[p.W + p.H + i] = p.floor_rays[(int64_t)i * p.W * 3 + 2];
     }
   }
-  if (p.mode == PXR_MODE_VIDEO) {  // nearest_map, distractor.py:179-181
-    for (int i = tid; i < p.H; i += kThreads)
+  if (p.mode == PXR_MODE_VIDEO && warp < kWarps - 1) {  // nearest_map, distractor.py:179-181
+    for (int i = tid; i < p.H; i += kSetupThreads)
       s_rowmap[i] = (uint32_t)(((int64_t)i * p.Hv) / p.H) * p.Wv * 3;
-    for (int i = tid; i < p.W; i += kThreads)
+    for (int i = tid; i < p.W; i += kSetupThreads)
       s_colmap[i] = (uint32_t)(((int64_t)i * p.Wv) / p.W) * 3;
   }
   if (tid == 0) {
@@ -608,9 +602,9 @@ render_step_kernel(const RenderParams p) {
   // output word from two consecutive source words -> 2 loads + one PRMT.
   const bool use_plan = p.mode == PXR_MODE_VIDEO && p.vframe_bulk && (p.W & 3) == 0 &&
                         ((p.Wv * 3) & 3) == 0;
-  if (use_plan) {
+  if (use_plan && warp < kWarps - 1) {
     int bad = 0;
-    for (int gc = tid; gc < (p.W >> 2); gc += kThreads) {
+    for (int gc = tid; gc < (p.W >> 2); gc += kSetupThreads) {
       const int x0 = gc * 4;
       const uint32_t base_word = s_colmap[x0] >> 2;
       uint4 pl;
@@ -642,21 +636,7 @@ render_step_kernel(const RenderParams p) {
   __syncthreads();
   const bool plan_ok = use_plan && es.plan_ok == 0;
 
-  // split env: this CTA renders band `band0` of env blockIdx.x / split
-  const int band0 = p.split > 1 ? (int)(blockIdx.x % (unsigned)p.split) : 0;
-  const int64_t env_first = p.split > 1 ? (int64_t)(blockIdx.x / (unsigned)p.split) : blockIdx.x;
-  if (warp == kWarps - 1 && env_first < p.batch)
-    prepare_env(p, env_first, 0, s_link, s_dist, es, lane, p.split == 1);
   __syncthreads();
-  if (p.split > 1) {
-    // every band has read the env's distractor state: band 0 writes its step
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (band0 == 0 && p.advance && warp == kWarps - 1 && lane == 0) {
-      DistSlot unused;
-      distractor_update(p, env_first, unused, true);
-    }
-  }
   PXR_PROF(0);  // once per CTA: setup + the first env's preparation
 
   // liveness: each thread owns a contiguous block of triangles (index order)
@@ -732,7 +712,7 @@ render_step_kernel(const RenderParams p) {
 
   uint32_t vphase = 0;
   int local_env = 0;
-  for (int64_t env = env_first; env < p.batch; env += p.env_stride, local_env++) {
+  for (int64_t env = blockIdx.x; env < p.batch; env += gridDim.x, local_env++) {
     // ---- phase 0: video fetch (the env's link trig, camera and distractor
     // state were prepared by warp kWarps-1 during the previous env) -------
     const int cb = local_env & 1;
@@ -744,7 +724,7 @@ render_step_kernel(const RenderParams p) {
                     (uint32_t)p.vframe_bytes, &es.vbar);
     }
     const float ex = es.ex[cb], ez = es.ez[cb];
-    bool prepared = env + p.env_stride >= p.batch;  // nothing to prepare for a last env
+    bool prepared = env + gridDim.x >= p.batch;  // nothing to prepare for a last env
 
     // the first liveness triangle's indices, loaded before the vertex phase
     // so their latency (L2: the geometry does not stay in the small L1 next
@@ -766,8 +746,7 @@ render_step_kernel(const RenderParams p) {
     // ---- bands of rows: everything below runs once per band (one band
     // whenever the frame's per-pixel state fits shared memory) ------------
     const int band_h = kBands ? p.band_h : p.H;
-    const int ystart = kBands ? band0 * band_h : 0;  // a split env: this CTA's band only
-    int yb = ystart;
+    int yb = 0;
     do {  // (no loop at all for one band)
       const int y0 = kBands ? yb : 0;  // compile-time 0 for one band
       const int y1 = kBands ? min(y0 + band_h, p.H) : p.H;
@@ -796,7 +775,7 @@ render_step_kernel(const RenderParams p) {
         else
           put_rgb(s_col, pix, rgb);
       };
-      if (kBands && y0 > ystart) {  // the previous band's TMA store must have finished reading
+      if (kBands && y0 > 0) {  // the previous band's TMA store must have finished reading
         if (tid == 0 && p.use_bulk) bulk_wait_read();
         __syncthreads();
       }
@@ -805,7 +784,7 @@ render_step_kernel(const RenderParams p) {
       // each thread's block of triangles (t0, t1) is contiguous, so its live
       // count and bbox-row total feed the block scan directly
       int my_live = 0, my_rows = 0;
-      if (kBands && y0 > ystart && t0 < t1) {  // (the first band's were loaded at the env's start)
+      if (kBands && y0 > 0 && t0 < t1) {  // (the first band's were loaded at the env's start)
         n0 = __ldg(p.tris + 3 * t0 + 0);
         n1 = __ldg(p.tris + 3 * t0 + 1);
         n2 = __ldg(p.tris + 3 * t0 + 2);
@@ -850,9 +829,9 @@ render_step_kernel(const RenderParams p) {
       // a floor (cheap texel / sky pixels) it is written by the warps the
       // records phase leaves idle (see below), else here by every thread:
       // threads first, first + stride, ...
-      const bool vwait = y0 == ystart && p.mode == PXR_MODE_VIDEO && p.vframe_bulk;
+      const bool vwait = y0 == 0 && p.mode == PXR_MODE_VIDEO && p.vframe_bulk;
       const uint32_t vpar = vphase;
-      if (y0 == ystart) vphase ^= 1u;  // the env's video frame (one fetch for all bands)
+      if (y0 == 0) vphase ^= 1u;  // the env's video frame (one fetch for all bands)
       auto background = [&](int first, int stride) {
         if (vwait) mbar_wait_parity(&es.vbar, vpar);
         if (p.mode == PXR_MODE_VIDEO && !kFloor && plan_ok && !p.gray) {
@@ -1148,7 +1127,7 @@ render_step_kernel(const RenderParams p) {
         // the other warps only (it would otherwise finish last)
         const int n_workers = prepared ? kWarps : kWarps - 1;
         if (warp == kWarps - 1 && !prepared) {
-          prepare_env(p, env + p.env_stride, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
+          prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
                       lane);
           prepared = true;
         }
@@ -1346,7 +1325,7 @@ render_step_kernel(const RenderParams p) {
         r0 = r1;
       }
       if (warp == kWarps - 1 && !prepared)  // env without live triangles
-        prepare_env(p, env + p.env_stride, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es, lane);
+        prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es, lane);
 
       // ---- depth output (debug / _render_frame parity only) ---------------
       if (p.out_depth != nullptr) {
@@ -1374,11 +1353,13 @@ render_step_kernel(const RenderParams p) {
         __syncthreads();
       }
       yb += band_h;
-    } while (kBands && p.split == 1 && yb < p.H);
+    } while (kBands && yb < p.H);
   }
-  if (tid == 0 && p.use_bulk) bulk_wait_all();
+  // the last frame store must have read shared memory before the CTA exits
+  // (its global writes complete with the grid)
+  if (tid == 0 && p.use_bulk) bulk_wait_read();
   if (p.prof != nullptr) {
-    PXR_PROF(7);  // the last store's completion
+    PXR_PROF(7);  // the last store's shared-memory read
     if (tid == 0) es.prof[8] = local_env;
     __syncthreads();
     if (tid < kProfSlots) p.prof[blockIdx.x * kProfSlots + tid] = es.prof[tid];
@@ -1594,26 +1575,6 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
       if (smem_layout(p).total <= budget) break;
     }
     if (debug_band > 0 && debug_band < bh) bh = debug_band;
-    // Small batches (at least two SMs per env): each env is split over a
-    // thread-block cluster of up to 8 CTAs, one row band each, so the
-    // latency-bound single-env chain runs on several SMs (the raster and
-    // background work divide by the band count; vertices and liveness are
-    // recomputed per band).
-    p.split = 1;
-    const int64_t dsplit = debug_int(kDbgSplit, -1);  // 0: never; n > 0: force n bands
-    if (dsplit != 0 && bh == height && p.stats == nullptr && debug_grid == 0) {
-      int64_t want = dsplit > 0 ? dsplit : (batch * 2 <= dev.num_sms ? dev.num_sms / batch : 1);
-      if (want > 8) want = 8;
-      if (want > 1) {
-        int sb = (int)((height + want - 1) / want);
-        if (sb % m) sb += m - sb % m;
-        const int nb = (height + sb - 1) / sb;
-        if (nb >= 2) {
-          p.split = nb;
-          bh = sb;
-        }
-      }
-    }
     p.band_h = bh;
     if (bh < height && (bh * bytes_row) % 16 != 0) p.use_bulk = 0;
     if (bh < height && (bh * width) % 4 != 0) p.depth_vec = 0;
@@ -1642,25 +1603,6 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   int64_t grid = (int64_t)dev.num_sms * per_sm;
   if (debug_grid > 0 && debug_grid < grid) grid = debug_grid;
   if (grid > batch) grid = batch;
-  if (p.split > 1) {  // one cluster of `split` CTAs per env
-    p.env_stride = batch;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(batch * p.split));
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = (size_t)smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)p.split;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, p);
-    if (e != cudaSuccess) return set_cuda(e, "render_step_kernel (cluster launch)");
-    return check_launch("render_step_kernel");
-  }
-  p.env_stride = grid;
   kernel<<<(unsigned)grid, kThreads, smem, st>>>(p);
   return check_launch("render_step_kernel");
 }

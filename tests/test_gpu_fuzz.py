@@ -34,10 +34,9 @@ def _case(seed):
 @pytest.mark.parametrize("seed", range(int(os.environ.get("PXR_FUZZ_SEEDS", "40"))))
 def test_fused_render_fuzz_vs_oracle(pkg, torch, oracle, knobs, seed):
     rng, name, mode, H, W, band, offset, fov, fib, gray, hv, wv = _case(seed)
-    # every third seed: each env split over a cluster of CTAs (row bands,
-    # the small-batch launch); else 1-4 persistent CTAs, several envs each
-    if seed % 3:
-        knobs.set("PXR_DEBUG_GRID", 1 + seed % 4)
+    # one env per CTA, or 1-3 CTAs rendering several envs each
+    if seed % 4:
+        knobs.set("PXR_DEBUG_GRID", seed % 4)
     if band:
         knobs.set("PXR_DEBUG_BAND_H", str(band))
     from paper_2502_00021_b200.models import forward_kinematics_host

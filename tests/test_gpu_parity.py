@@ -104,21 +104,15 @@ class TestDeviceMath:
 
 
 class TestRenderGolden:
-    @pytest.mark.parametrize("launch", ["auto", "grid3", "split8", "nosplit"])
+    @pytest.mark.parametrize("grid", [0, 3])
     @pytest.mark.parametrize("name", MODEL_NAMES)
-    def test_frames_exact(self, torch, pkg, knobs, name, launch):
-        """Golden frames (40 envs) through each launch shape: the default
-        (each env split over a cluster of CTAs, one row band each), 8 bands
-        per env, one env per CTA, and at most 3 CTAs (every CTA renders
-        several envs: the cross-env prefetch of link trig and distractor slot,
-        the double-buffered link table, the video mbarrier parity flip, the
-        TMA store overlapping the next env)."""
-        if launch == "grid3":
-            knobs.set("PXR_DEBUG_GRID", 3)
-        elif launch == "split8":
-            knobs.set("PXR_DEBUG_SPLIT", 8)
-        elif launch == "nosplit":
-            knobs.set("PXR_DEBUG_SPLIT", 0)
+    def test_frames_exact(self, torch, pkg, knobs, name, grid):
+        """Golden frames with one env per CTA, and with at most 3 CTAs (every
+        CTA renders several envs: the cross-env prefetch of link trig and
+        distractor slot, the double-buffered link table, the video mbarrier
+        parity flip, the TMA store overlapping the next env)."""
+        if grid:
+            knobs.set("PXR_DEBUG_GRID", grid)
         rec = golden(f"render_{name}.npz")
         geom = geometry_of(name)
         poses = to_dev(torch, rec["poses"])
@@ -318,16 +312,11 @@ def fused_replay(torch, pkg, tag):
         np.testing.assert_array_equal(host["direction"], rec["final_direction"])
 
 
-@pytest.mark.parametrize("launch", ["auto", "grid3", "nosplit"])
+@pytest.mark.parametrize("grid", [0, 3])
 @pytest.mark.parametrize("tag", REPLAYS)
-def test_fused_replay_hash_chain(torch, pkg, knobs, tag, launch):
-    """The reference's recorded chains through the fused step: the default
-    launch (small batches: each env split over a cluster, the distractor
-    step written once per cluster), several envs per CTA, one env per CTA."""
-    if launch == "grid3":
-        knobs.set("PXR_DEBUG_GRID", 3)
-    elif launch == "nosplit":
-        knobs.set("PXR_DEBUG_SPLIT", 0)
+def test_fused_replay_hash_chain(torch, pkg, knobs, tag, grid):
+    if grid:  # several envs per CTA
+        knobs.set("PXR_DEBUG_GRID", grid)
     fused_replay(torch, pkg, tag)
 
 
