@@ -189,6 +189,10 @@ pxr_status pxr_sincosf(const float *x, float *s, float *c, int64_t n, void *stre
  * the parity test. */
 pxr_status pxr_sincos(const double *x, double *s, double *c, int64_t n, void *stream);
 
+/* Device log in float64 (numpy's AVX-512 log restated: the reset draws'
+ * Box-Muller log) for the parity test. */
+pxr_status pxr_log(const double *x, double *y, int64_t n, void *stream);
+
 /* Synthetic pose source for benchmarking: per env g =
  * env_offset + i, qpos = rest + U(-0.1, 0.1) from the reference reset keys
  * plus a deterministic joint oscillation at step t, then planar forward

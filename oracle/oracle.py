@@ -48,6 +48,16 @@ def sincos64(x):
     return s, c
 
 
+def np_log(x):
+    """numpy's AVX-512 float64 log (np_log_svml.c restatement); positive
+    normal inputs."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    dp = ctypes.POINTER(ctypes.c_double)
+    lib().np_log_svml_batch(x.ctypes.data_as(dp), y.ctypes.data_as(dp), x.size)
+    return y
+
+
 def build() -> str:
     """Compile liboracle.so with the committed Makefile (idempotent)."""
     subprocess.run(["make", "-s", "-C", _HERE], check=True)
@@ -68,6 +78,8 @@ def lib():
         L.oracle_sincosf_selftest.argtypes = [ctypes.c_uint32] * 3
         L.oracle_sincosf_many.restype = None
         L.oracle_sincosf_many.argtypes = [_f32p, _f32p, _f32p, _I64]
+        L.np_log_svml_batch.restype = None
+        L.np_log_svml_batch.argtypes = [ctypes.POINTER(ctypes.c_double)] * 2 + [_I64]
         L.glibc_sincos_batch.restype = None
         L.glibc_sincos_batch.argtypes = [ctypes.POINTER(ctypes.c_double)] * 3 + [_I64]
         L.oracle_threefry2x64.restype = None

@@ -32,7 +32,7 @@ EXPORTED = (
     "pxr_apply_color", "pxr_apply_video", "pxr_grayscale", "pxr_threefry2x64",
     "pxr_sincosf", "pxr_pose_source", "pxr_forward_kinematics", "pxr_div_check",
     "pxr_physics_step", "pxr_reset_envs", "pxr_env_poses", "pxr_conv_stub_forward",
-    "pxr_step_key_advance", "pxr_set_debug", "pxr_sincos",
+    "pxr_step_key_advance", "pxr_set_debug", "pxr_sincos", "pxr_log",
 )
 
 _vp = ctypes.c_void_p
@@ -143,6 +143,8 @@ def lib() -> ctypes.CDLL:
     L.pxr_div_check.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp]
     L.pxr_sincosf.restype = _i32
     L.pxr_sincosf.argtypes = [_vp, _vp, _vp, _i64, _vp]
+    L.pxr_log.restype = _i32
+    L.pxr_log.argtypes = [_vp, _vp, _i64, _vp]
     L.pxr_sincos.restype = _i32
     L.pxr_sincos.argtypes = [_vp, _vp, _vp, _i64, _vp]
     L.pxr_pose_source.restype = _i32

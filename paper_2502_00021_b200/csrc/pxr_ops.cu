@@ -22,6 +22,7 @@
 #include "../../include/pxr.h"
 #include "pxr_internal.cuh"
 #include "pxr_glibc_sincos.cuh"
+#include "pxr_numpy_log.cuh"
 #include "pxr_math.cuh"
 
 namespace pxr {
@@ -488,6 +489,19 @@ __global__ void sincos64_kernel(const double *x, double *s, double *c, int64_t n
     s[i] = glibc_sin(v);
     c[i] = glibc_cos(v);
   }
+}
+
+__global__ void log64_kernel(const double *x, double *y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = numpy_log(x[i]);
+}
+
+extern "C" pxr_status pxr_log(const double *x, double *y, int64_t n, void *stream) {
+  if (n < 0 || (n > 0 && (x == nullptr || y == nullptr))) return set_invalid("bad log args");
+  if (n == 0) return PXR_OK;
+  log64_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, y, n);
+  return check_launch("log64_kernel");
 }
 
 extern "C" pxr_status pxr_sincos(const double *x, double *s, double *c, int64_t n, void *stream) {

@@ -17,10 +17,9 @@
 // and the f64 sin / cos are glibc's, restated (pxr_glibc_sincos.cuh), so
 // dynamics, rewards, FK and the reset qpos draws are bit-identical to the
 // reference (tests/test_env_gpu.py, test_physics_api.py; the recorded
-// reference rollouts reproduce in full, tests/test_recorder.py). The one
-// remaining difference is the log of the reset qvel Box-Muller draw
-// (prng.py:138-152): numpy evaluates it with its AVX-512 SVML log, the
-// device with CUDA's; they differ in the last bit on ~1 % of draws.
+// reference rollouts reproduce in full, tests/test_recorder.py). The log of
+// the reset qvel Box-Muller draw (prng.py:138-152) is numpy's AVX-512 SVML
+// log, restated in pxr_numpy_log.cuh.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -29,6 +28,7 @@
 #include "../../include/pxr.h"
 #include "pxr_internal.cuh"
 #include "pxr_glibc_sincos.cuh"
+#include "pxr_numpy_log.cuh"
 #include "pxr_math.cuh"
 
 namespace pxr {
@@ -556,7 +556,7 @@ __device__ void normal_draws(uint64_t khi, uint64_t klo, int n, double *out) {
   for (int i = 0; i < mm; i++) {
     const double u1 = ((double)(bits[i] >> 11) + 1.0) * 0x1p-53;
     const double u2 = (double)(bits[mm + i] >> 11) * 0x1p-53;
-    const double r = sqrt(-2.0 * log(u1));
+    const double r = sqrt(-2.0 * numpy_log(u1));  // np.log: numpy's SVML log
     const double th = 2.0 * 3.141592653589793 * u2;
     if (i < n) out[i] = r * glibc_cos(th);
     if (mm + i < n) out[mm + i] = r * glibc_sin(th);

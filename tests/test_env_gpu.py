@@ -3,10 +3,8 @@
 Observations are bit-exact for a given state (the hot-path contract).
 Physics reproduces the reference's operation order with glibc's f64 sin /
 cos restated on the device, so dynamics, rewards, FK and reset qpos draws
-are bit-exact. The reset qvel draws' Box-Muller log
-is numpy's AVX-512 SVML log on the reference host, not glibc's; CUDA's log
-differs from it in the last bit on ~1 % of draws, so qvel is compared to
-1e-13 relative."""
+are bit-exact; so are the reset qvel draws, whose
+Box-Muller log is numpy's own AVX-512 (SVML) log, restated on the device."""
 
 import dataclasses
 import os
@@ -74,8 +72,7 @@ class TestPhysics:
 
         sys, _, _ = E._reset_state(env, fold_in(key_from_seed(3), 0x5EED))
         np.testing.assert_array_equal(sys.qpos.cpu().numpy(), rec[f"{name}_reset_qpos"])
-        np.testing.assert_allclose(sys.qvel.cpu().numpy(), rec[f"{name}_reset_qvel"],
-                                   rtol=1e-13, atol=1e-15)
+        np.testing.assert_array_equal(sys.qvel.cpu().numpy(), rec[f"{name}_reset_qvel"])
 
 
 REPLAYS = ("cheetah_none_b1", "walker_video_b8", "ant_color_b8",

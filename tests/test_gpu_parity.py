@@ -63,6 +63,19 @@ class TestDeviceMath:
         np.testing.assert_array_equal(s.cpu().numpy(), np.sin(x))
         np.testing.assert_array_equal(c.cpu().numpy(), np.cos(x))
 
+    def test_log64_matches_numpy_restatement(self, torch, pkg, oracle):
+        """Device numpy-SVML log (the reset draws' Box-Muller log) against
+        the CPU twin, which tests/test_oracle.py pins to np.log."""
+        rng = np.random.default_rng(4)
+        w = rng.integers(0, 2**63, 1 << 21, dtype=np.int64).astype(np.uint64)
+        u = ((w >> np.uint64(11)).astype(np.float64) + 1.0) * 2.0 ** -53  # prng.py:145
+        x = np.concatenate([u, np.exp(rng.uniform(np.log(1e-300), np.log(1e300), 1 << 21))])
+        xd = to_dev(torch, x)
+        y = torch.empty_like(xd)
+        pkg._native.check(pkg._native.lib().pxr_log(xd.data_ptr(), y.data_ptr(), xd.numel(),
+                                                    pkg._native.stream_ptr()))
+        np.testing.assert_array_equal(y.cpu().numpy(), oracle.np_log(x))
+
     def test_exact_division(self, torch, pkg):
         """The raster's division (per-triangle RN reciprocal + one Markstein
         correction) must equal IEEE a / b for every operand it can see."""

@@ -84,6 +84,23 @@ class TestOracleSinCos64:
         np.testing.assert_array_equal(c, np.cos(x))
 
 
+class TestOracleNumpyLog:
+    """oracle/np_log_svml.c (numpy 2.3.5's AVX-512 float64 log, the
+    Box-Muller log of the reset draws, prng.py:147) against np.log."""
+
+    def test_matches_numpy(self, oracle):
+        rng = np.random.default_rng(5)
+        for lo, hi in ((2.0 ** -53, 1.0), (0.5, 2.0), (1e-300, 1e300)):
+            x = np.exp(rng.uniform(np.log(lo), np.log(hi), 4_000_000))
+            np.testing.assert_array_equal(oracle.np_log(x), np.log(x))
+
+    def test_uniform_draws(self, oracle):
+        # the reset draws' own arguments: (w >> 11) 2^-53 in [2^-53, 1)
+        w = np.random.default_rng(6).integers(0, 2**63, 2_000_000, dtype=np.int64)
+        u = ((w.astype(np.uint64) >> np.uint64(11)) | np.uint64(1)).astype(np.float64) * 2.0 ** -53
+        np.testing.assert_array_equal(oracle.np_log(u), np.log(u))
+
+
 class TestOracleRender:
     @pytest.mark.parametrize("name", MODEL_NAMES)
     def test_matches_reference_frames(self, oracle, name):
