@@ -1041,6 +1041,10 @@ render_step_kernel(const RenderParams p) {
         const bool bg_split = bg_here && rec_warps <= kWarps - 4;
         for (int li = r0 + tid; li < r1; li += kThreads) {
           const int t = s_ids[li];
+          // the flat colour's L2 loads first: issued after the sqrtf's slow-
+          // path branch they stalled the shading below by a full L2 latency
+          const float tc0 = __ldg(p.tri_colors + 3 * t + 0), tc1 = __ldg(p.tri_colors + 3 * t + 1),
+                      tc2 = __ldg(p.tri_colors + 3 * t + 2);
           int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
               i2 = __ldg(p.tris + 3 * t + 2);
           const float2 a = s_vxy32[i0];
@@ -1058,8 +1062,10 @@ render_step_kernel(const RenderParams p) {
           const double ndotl = nd32 < 0.0f ? 0.0 : (double)nd32;
           const double shade = 0.35 + 0.65 * ndotl;
           uint32_t rgb = 0;
+          const float tcol[3] = {tc0, tc1, tc2};
+#pragma unroll
           for (int ch = 0; ch < 3; ch++) {
-            double v = (double)__ldg(p.tri_colors + 3 * t + ch) * shade * 255.0;
+            double v = (double)tcol[ch] * shade * 255.0;
             if (v > 255.0) v = 255.0;
             rgb |= ((uint32_t)v & 0xffu) << (8 * ch);
           }
@@ -1132,6 +1138,18 @@ render_step_kernel(const RenderParams p) {
           prepared = true;
         }
         uint2 *q = s_queue + warp * 64;
+        // a covered candidate: min-reduce its f32 depth into the pixel and
+        // take a fragment-list slot (ptxas aggregates the warp's increments
+        // into one shared atomic)
+        auto add_fragment = [&](double z, uint32_t pix, int tri) {
+          const int slot = atomicAdd(&es.n_frag, 1);
+          const float zf = (float)z;
+          const uint32_t zb = __float_as_uint(zf);
+          if (zb < atomicMin(&s_dbits[pix], zb)) atomicOr(&s_wkey[pix], kDecBit);
+          if (slot < p.frag_limit)
+            s_frag[slot] = make_uint2(zb | (z < (double)zf ? 0x80000000u : 0u),
+                                      pix | ((uint32_t)tri << 20));
+        };
         int qn = 0;  // queued spans (warp-uniform)
         bool more = true;
         int k = warp - n_workers;
@@ -1183,15 +1201,32 @@ render_step_kernel(const RenderParams p) {
               j = (int)(sp.y >> 16);
             }
             __syncwarp();
-            // expand the 32 spans into pixel candidates
+            if (more) {
+              // steady state (32 spans queued): each lane tests the first
+              // pixel of its own span -- a full round of 32 candidates with
+              // no expansion scan or owner search -- and re-queues the span's
+              // remaining pixels (most spans hold one pixel)
+              PXR_DCHECK(nb == 32 && len > 0);
+              if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[3], 32);
+              const uint32_t pix = (uint32_t)((row - y0) * p.W + x0);
+              PXR_DCHECK(pix < (uint32_t)npx && j < n_round);
+              double z;
+              if (eval_exact(s_rec[j], x0, row, s_vxy64, s_viz, z)) add_fragment(z, pix, j);
+              const bool keep = len > 1;
+              const uint32_t km = __ballot_sync(kFull, keep);
+              if (keep)
+                q[qn + __popc(km & lanemask_lt)] =
+                    make_uint2((uint32_t)(x0 + 1) | ((uint32_t)(len - 1) << 16),
+                               (uint32_t)row | ((uint32_t)j << 16));
+              qn += __popc(km);
+              PXR_DCHECK(qn <= kQueue);
+              continue;
+            }
+            // draining the queue: expand the spans into pixel candidates
             const int incl = warp_incl_scan(len, lane);
             const int excl = incl - len;
             const int N = __shfl_sync(kFull, incl, 31);
-            // while spans keep coming only whole rounds of 32 candidates are
-            // evaluated; the rest of the batch goes back on the queue (most
-            // spans hold one pixel, so a batch is ~34 candidates: without
-            // this every batch would end with a nearly empty round)
-            const int NE = more ? (N & ~31) : N;
+            const int NE = N;
             if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[3], NE);
             for (int c0 = 0; c0 < NE; c0 += 32) {
               // span lane of candidate c = c0 + lane: the number of lanes whose
@@ -1216,28 +1251,7 @@ render_step_kernel(const RenderParams p) {
                 PXR_DCHECK(pix < (uint32_t)npx && o_tri < n_round && owner < 32);
                 cov = eval_exact(s_rec[o_tri], px, o_row, s_vxy64, s_viz, z);
               }
-              if (cov) {
-                // a unique list slot per covered lane (ptxas aggregates the
-                // warp's increments into one shared atomic)
-                const int slot = atomicAdd(&es.n_frag, 1);
-                const float zf = (float)z;
-                const uint32_t zb = __float_as_uint(zf);
-                if (zb < atomicMin(&s_dbits[pix], zb)) atomicOr(&s_wkey[pix], kDecBit);
-                if (slot < p.frag_limit)
-                  s_frag[slot] = make_uint2(zb | (z < (double)zf ? 0x80000000u : 0u),
-                                            pix | ((uint32_t)o_tri << 20));
-              }
-            }
-            if (NE < N) {  // (nb == 32 here, so NE >= 32: progress)
-              const int skip = max(NE - excl, 0);  // pixels of this span already done
-              const bool keep = incl > NE;
-              const uint32_t km = __ballot_sync(kFull, keep);
-              if (keep)
-                q[qn + __popc(km & lanemask_lt)] =
-                    make_uint2((uint32_t)(x0 + skip) | ((uint32_t)(len - skip) << 16),
-                               (uint32_t)row | ((uint32_t)j << 16));
-              qn += __popc(km);
-              PXR_DCHECK(qn <= kQueue);
+              if (cov) add_fragment(z, pix, o_tri);
             }
           }
         }
