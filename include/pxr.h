@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PXR_ABI_VERSION 2
+#define PXR_ABI_VERSION 3
 
 typedef int32_t pxr_status;
 #define PXR_OK 0
@@ -87,6 +87,12 @@ typedef struct pxr_video_pack {
   const int64_t *starts;   /* (n_videos) first frame of each video          */
   const int64_t *counts;   /* (n_videos) frame count of each video          */
   int64_t n_videos, n_frames, height, width;
+  /* optional: every frame already nearest-upscaled to the observation size
+   * (pxr_pack_upscale; NULL if absent). pxr_render_step then copies the env's
+   * frame into its RGB frame buffer with one TMA bulk load instead of
+   * gathering texels per pixel (same bytes: distractor.py:172-181). */
+  const uint8_t *frames_hw;  /* (n_frames, hw_height, hw_width, 3) u8       */
+  int64_t hw_height, hw_width;
 } pxr_video_pack;
 
 /* Per-step key material (env.py:176-255). */
@@ -111,7 +117,7 @@ const char *pxr_status_string(pxr_status s);
 const char *pxr_last_error(void);
 /* Test / debug knobs (no reference counterpart): `name` is one of
  * PXR_DEBUG_FRAG_LIMIT, _ROW_CAP, _CAP, _STATS_PTR, _BAND_H, _NO_PACKED_SCAN,
- * _PHYS, _GRID, _PROF; `value` its string value, NULL to unset. The PXR_DEBUG_*
+ * _PHYS, _GRID, _PROF, _NO_UPSCALE; `value` its string value, NULL to unset. The PXR_DEBUG_*
  * environment is read once at the first query; this overrides it. */
 pxr_status pxr_set_debug(const char *name, const char *value);
 
@@ -181,6 +187,12 @@ pxr_status pxr_threefry2x64(const uint64_t *k0, const uint64_t *k1, int64_t key_
  * next to IEEE a / b, for the parity test. */
 pxr_status pxr_div_check(const double *a, const double *b, double *q_pre, double *q_ieee,
                          int64_t n, void *stream);
+
+/* nearest_map compositing source (distractor.py:172-181) precomputed once
+ * per pack and observation size: out[f][y][x] = frames[f][(y*Hv)//H][(x*Wv)//W]
+ * for every frame f, out (n_frames, height, width, 3) u8. */
+pxr_status pxr_pack_upscale(const pxr_video_pack *pack, int64_t height, int64_t width,
+                            uint8_t *out, void *stream);
 
 /* Device sinf/cosf (glibc 2.39 restatement) for the parity test. */
 pxr_status pxr_sincosf(const float *x, float *s, float *c, int64_t n, void *stream);

@@ -32,7 +32,7 @@ EXPORTED = (
     "pxr_apply_color", "pxr_apply_video", "pxr_grayscale", "pxr_threefry2x64",
     "pxr_sincosf", "pxr_pose_source", "pxr_forward_kinematics", "pxr_div_check",
     "pxr_physics_step", "pxr_reset_envs", "pxr_env_poses", "pxr_conv_stub_forward",
-    "pxr_step_key_advance", "pxr_set_debug", "pxr_sincos", "pxr_log",
+    "pxr_step_key_advance", "pxr_set_debug", "pxr_sincos", "pxr_log", "pxr_pack_upscale",
 )
 
 _vp = ctypes.c_void_p
@@ -67,6 +67,7 @@ class VideoPackC(ctypes.Structure):
     _fields_ = [
         ("frames", _vp), ("starts", _vp), ("counts", _vp), ("n_videos", _i64),
         ("n_frames", _i64), ("height", _i64), ("width", _i64),
+        ("frames_hw", _vp), ("hw_height", _i64), ("hw_width", _i64),
     ]
 
 
@@ -143,6 +144,8 @@ def lib() -> ctypes.CDLL:
     L.pxr_div_check.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp]
     L.pxr_sincosf.restype = _i32
     L.pxr_sincosf.argtypes = [_vp, _vp, _vp, _i64, _vp]
+    L.pxr_pack_upscale.restype = _i32
+    L.pxr_pack_upscale.argtypes = [P(VideoPackC), _i64, _i64, _vp, _vp]
     L.pxr_log.restype = _i32
     L.pxr_log.argtypes = [_vp, _vp, _i64, _vp]
     L.pxr_sincos.restype = _i32
@@ -165,8 +168,8 @@ def lib() -> ctypes.CDLL:
     L.pxr_env_poses.argtypes = [P(Model), _vp, _i64, _vp, _vp]
     L.pxr_set_debug.restype = _i32
     L.pxr_set_debug.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
-    if L.pxr_abi_version() != 2:
-        raise ImportError(f"{LIB_PATH}: ABI version {L.pxr_abi_version()} != 2")
+    if L.pxr_abi_version() != 3:
+        raise ImportError(f"{LIB_PATH}: ABI version {L.pxr_abi_version()} != 3")
     _lib = L
     return L
 

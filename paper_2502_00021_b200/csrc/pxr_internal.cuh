@@ -55,6 +55,7 @@ enum DebugKnob {
   kDbgPhys,          // PXR_DEBUG_PHYS: warp|half|quarter|thread physics kernel
   kDbgGrid,          // PXR_DEBUG_GRID: at most this many CTAs (several envs per CTA)
   kDbgProf,          // PXR_DEBUG_PROF: device int64 (grid, 12) per-CTA phase cycles
+  kDbgNoUpscale,     // PXR_DEBUG_NO_UPSCALE: gather video texels even with an upscaled pack
   kDbgCount
 };
 // value of a knob, or nullptr when unset

@@ -42,7 +42,7 @@ pxr_status set_cuda(cudaError_t e, const char *where) {
 static const char *const kKnobNames[kDbgCount] = {
     "PXR_DEBUG_FRAG_LIMIT", "PXR_DEBUG_ROW_CAP",        "PXR_DEBUG_CAP",  "PXR_DEBUG_STATS_PTR",
     "PXR_DEBUG_BAND_H",     "PXR_DEBUG_NO_PACKED_SCAN", "PXR_DEBUG_PHYS", "PXR_DEBUG_GRID",
-    "PXR_DEBUG_PROF"};
+    "PXR_DEBUG_PROF",       "PXR_DEBUG_NO_UPSCALE"};
 static std::mutex g_knob_mu;
 static std::string g_knob_val[kDbgCount];
 static bool g_knob_set[kDbgCount];
@@ -472,6 +472,33 @@ extern "C" pxr_status pxr_step_key_advance(uint64_t master_hi, uint64_t master_l
   if (t == nullptr || key_out == nullptr) return set_invalid("pxr_step_key_advance: null argument");
   step_key_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(master_hi, master_lo, t, key_out);
   return check_launch("step_key_kernel");
+}
+
+__global__ void pack_upscale_kernel(const uint8_t *frames, int64_t n_frames, int Hv, int Wv,
+                                    int H, int W, uint8_t *out) {
+  const int64_t n = n_frames * H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = i / ((int64_t)H * W);
+    const int r = (int)(i - f * H * W), y = r / W, x = r - y * W;
+    const uint8_t *src = frames + ((f * Hv + ((int64_t)y * Hv) / H) * Wv + ((int64_t)x * Wv) / W) * 3;
+    out[i * 3 + 0] = src[0];
+    out[i * 3 + 1] = src[1];
+    out[i * 3 + 2] = src[2];
+  }
+}
+
+extern "C" pxr_status pxr_pack_upscale(const pxr_video_pack *pack, int64_t height, int64_t width,
+                                       uint8_t *out, void *stream) {
+  if (pack == nullptr || pack->frames == nullptr || out == nullptr)
+    return set_invalid("pxr_pack_upscale: null pointers");
+  if (height < 1 || width < 1 || pack->height < 1 || pack->width < 1 || pack->n_frames < 0)
+    return set_invalid("pxr_pack_upscale: bad sizes");
+  if (pack->n_frames == 0) return PXR_OK;
+  pack_upscale_kernel<<<blocks_for(pack->n_frames * height * width, 256), 256, 0,
+                        (cudaStream_t)stream>>>(pack->frames, pack->n_frames, (int)pack->height,
+                                                (int)pack->width, (int)height, (int)width, out);
+  return check_launch("pack_upscale_kernel");
 }
 
 extern "C" pxr_status pxr_sincosf(const float *x, float *s, float *c, int64_t n, void *stream) {

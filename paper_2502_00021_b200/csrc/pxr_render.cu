@@ -159,6 +159,10 @@ struct RenderParams {
   int row_cap;     // bbox rows per raster round
   int frag_limit;  // fragment list limit (kFragCap; test override)
   int frame_bytes, use_bulk, vframe_bytes, vframe_bulk;
+  // RGB video with the pack upscaled to the frame size: the env's upscaled
+  // frame is TMA-copied into the colour buffer as its background
+  const uint8_t *frames_hw;
+  int hw;
   uint32_t wmagic;  // ceil(2^32 / W): flat pixel index -> row
   int depth_vec;    // out_depth groups of 4 pixels are 16-byte aligned
   int band_h;       // rows per band: a frame is rendered in bands that fit shared memory
@@ -198,9 +202,10 @@ __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   L.col = o;    o += align_up(npx * 3, 16);
   L.wkey = o;   o += align_up(npx * 4, 16);
   L.gray = o;   o += p.gray ? align_up(npx, 16) : 0;
-  L.gplan = o;  o += p.mode == PXR_MODE_VIDEO ? align_up((p.W / 4 + 1) * 16, 16) : 0;
+  const bool gather = p.mode == PXR_MODE_VIDEO && !p.hw;  // texels gathered per pixel
+  L.gplan = o;  o += gather ? align_up((p.W / 4 + 1) * 16, 16) : 0;
   // + 32 B: the byte-permute gather may read up to 20 B past the last texel
-  L.vframe = o; o += p.mode == PXR_MODE_VIDEO ? align_up(p.vframe_bytes + 32, 16) : 0;
+  L.vframe = o; o += gather ? align_up(p.vframe_bytes + 32, 16) : 0;
   L.total = o;
   return L;
 }
@@ -600,7 +605,7 @@ render_step_kernel(const RenderParams p) {
   // W % 4 == 0 and 4-byte-aligned source rows, the 12 output bytes of a
   // 4-pixel group come from one 24-byte window of the source row, and each
   // output word from two consecutive source words -> 2 loads + one PRMT.
-  const bool use_plan = p.mode == PXR_MODE_VIDEO && p.vframe_bulk && (p.W & 3) == 0 &&
+  const bool use_plan = p.mode == PXR_MODE_VIDEO && !p.hw && p.vframe_bulk && (p.W & 3) == 0 &&
                         ((p.Wv * 3) & 3) == 0;
   if (use_plan && warp < kWarps - 1) {
     int bad = 0;
@@ -717,7 +722,7 @@ render_step_kernel(const RenderParams p) {
     // state were prepared by warp kWarps-1 during the previous env) -------
     const int cb = local_env & 1;
     if (kWithStats && p.stats != nullptr && tid < kStats) es.st[tid] = 0;
-    if (tid == 0 && p.mode == PXR_MODE_VIDEO && p.vframe_bulk) {
+    if (tid == 0 && p.mode == PXR_MODE_VIDEO && !p.hw && p.vframe_bulk) {
       PXR_DCHECK(es.frame_idx[cb] >= 0 && es.frame_idx[cb] < p.n_frames);
       mbar_arrive_expect_tx(&es.vbar, (uint32_t)p.vframe_bytes);
       bulk_load_g2s(s_vframe, p.frames + es.frame_idx[cb] * p.vframe_bytes,
@@ -775,6 +780,17 @@ render_step_kernel(const RenderParams p) {
         else
           put_rgb(s_col, pix, rgb);
       };
+      if (!kBands && p.hw && tid == 0) {
+        // the env's video frame, upscaled to the frame size, straight into the
+        // colour buffer (the previous store has read it: awaited before the
+        // vertex barrier); every pixel the resolve does not paint keeps it
+        // (distractor.py:172-176: covered pixels are painted, the rest keep
+        // the texel)
+        PXR_DCHECK(es.frame_idx[cb] >= 0 && es.frame_idx[cb] < p.n_frames);
+        mbar_arrive_expect_tx(&es.vbar, (uint32_t)p.frame_bytes);
+        bulk_load_g2s(s_col, p.frames_hw + es.frame_idx[cb] * p.frame_bytes,
+                      (uint32_t)p.frame_bytes, &es.vbar);
+      }
       if (kBands && y0 > 0) {  // the previous band's TMA store must have finished reading
         if (tid == 0 && p.use_bulk) bulk_wait_read();
         __syncthreads();
@@ -829,10 +845,22 @@ render_step_kernel(const RenderParams p) {
       // a floor (cheap texel / sky pixels) it is written by the warps the
       // records phase leaves idle (see below), else here by every thread:
       // threads first, first + stride, ...
-      const bool vwait = y0 == 0 && p.mode == PXR_MODE_VIDEO && p.vframe_bulk;
+      const bool vwait = y0 == 0 && p.mode == PXR_MODE_VIDEO && !p.hw && p.vframe_bulk;
       const uint32_t vpar = vphase;
       if (y0 == 0) vphase ^= 1u;  // the env's video frame (one fetch for all bands)
       auto background = [&](int first, int stride) {
+        if (!kBands && p.hw) {  // colours arrive by TMA: depth +inf, empty keys
+          const float inf = __int_as_float(0x7f800000);
+          for (int gi = first; gi < (npx >> 2); gi += stride) {
+            reinterpret_cast<float4 *>(s_depth)[gi] = make_float4(inf, inf, inf, inf);
+            reinterpret_cast<uint4 *>(s_wkey)[gi] = make_uint4(0u, 0u, 0u, 0u);
+          }
+          for (int i = ((npx >> 2) << 2) + first; i < npx; i += stride) {
+            s_depth[i] = inf;
+            s_wkey[i] = 0u;
+          }
+          return;
+        }
         if (vwait) mbar_wait_parity(&es.vbar, vpar);
         if (p.mode == PXR_MODE_VIDEO && !kFloor && plan_ok && !p.gray) {
           // 4-pixel groups: three texel words through the byte-permute plan
@@ -1257,6 +1285,8 @@ render_step_kernel(const RenderParams p) {
         }
         __syncthreads();
         PXR_PROF(4);  // row spans -> candidates -> exact test -> fragments
+        // the upscaled video frame must have landed before the paint
+        if (!kBands && p.hw && r0 == 0) mbar_wait_parity(&es.vbar, vpar);
 
         // exact sequential-order resolve (see the file header)
         const int n_frag = es.n_frag;
@@ -1357,6 +1387,8 @@ render_step_kernel(const RenderParams p) {
       uint8_t *gout = p.out + (int64_t)env * p.frame_bytes + (int64_t)y0 * p.W * chans;
       const int band_bytes = npx * chans;
       if (p.use_bulk) {  // host: every band's size and offset are multiples of 16
+        // (no live triangle: the frame copy has not been awaited yet)
+        if (!kBands && p.hw && n_live == 0 && tid == 0) mbar_wait_parity(&es.vbar, vpar);
         fence_proxy_async_smem();
         __syncthreads();
         PXR_PROF(6);  // paint (+ depth output)
@@ -1515,6 +1547,7 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     p.Hv = (int)pack->height;
     p.Wv = (int)pack->width;
     p.vframe_bytes = p.Hv * p.Wv * 3;
+    p.frames_hw = pack->frames_hw;
     p.vframe_bulk = (p.vframe_bytes % 16 == 0) &&
                     ((reinterpret_cast<uintptr_t>(pack->frames) & 15) == 0);
   }
@@ -1593,6 +1626,15 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     if (bh < height && (bh * bytes_row) % 16 != 0) p.use_bulk = 0;
     if (bh < height && (bh * width) % 4 != 0) p.depth_vec = 0;
   }
+  // RGB video, one band, the pack upscaled to this frame size: the env's
+  // background is one TMA copy of its upscaled frame (no texel gather, no
+  // raw-frame buffer in shared memory)
+  p.hw = 0;
+  if (mode == PXR_MODE_VIDEO && p.band_h == p.H && !p.gray && p.use_bulk &&
+      pack->frames_hw != nullptr && pack->hw_height == height && pack->hw_width == width &&
+      (reinterpret_cast<uintptr_t>(pack->frames_hw) & 15) == 0 &&
+      debug_knob(kDbgNoUpscale) == nullptr)
+    p.hw = 1;
   for (;;) {
     p.cap = cap;
     if (smem_layout(p).total <= budget || cap <= 16) break;

@@ -353,7 +353,9 @@ class RobotRenderer:
             out_depth = torch.empty((B, self.height, self.width), dtype=torch.float32,
                                     device=poses.device)
         dist_c = dist.c_struct() if dist is not None else _native.Distractor(_native.MODE_NONE)
-        pack_c = pack.c_struct() if pack is not None else None
+        # RGB video: the pack's frames upscaled to this renderer's size (TMA copy)
+        pack_c = (pack.c_struct(self.height, self.width) if not grayscale else pack.c_struct()) \
+            if pack is not None else None
         keys_c = keys
         done_p = _native.ptr(done)
         st = _native.stream_ptr(stream)

@@ -34,6 +34,10 @@ CONFIGS = [
     ("Walker2d", 4096, "video", True),     # grayscale composite
     ("Ant", 4096, "color", True),
 ]
+# RGB video takes the pack upscaled to the frame size (one TMA copy per env);
+# these run the per-pixel texel gather instead (PXR_DEBUG_NO_UPSCALE)
+GATHER = [("Humanoid", 4096, "video", False), ("Walker2d", 16384, "video", False)]
+CASES = [c + (False,) for c in CONFIGS] + [c + (True,) for c in GATHER]
 
 STEPS = 3
 DONE_RATE = 0.15
@@ -61,10 +65,14 @@ def _first_bad_env(a, b):
     return bad[:10]
 
 
-@pytest.mark.parametrize("model,B,mode,gray", CONFIGS,
-                         ids=[f"{m}-{b}-{d}{'-gray' if g else ''}" for m, b, d, g in CONFIGS])
-def test_fused_step_full_batch(torch, pkg, oracle, model, B, mode, gray):
+@pytest.mark.parametrize("model,B,mode,gray,gather", CASES,
+                         ids=[f"{m}-{b}-{d}{'-gray' if g else ''}{'-gather' if q else ''}"
+                              for m, b, d, g, q in CASES])
+def test_fused_step_full_batch(torch, pkg, oracle, knobs, model, B, mode, gray, gather):
     from paper_2502_00021_b200 import bench_support as bs
+
+    if gather:
+        knobs.set("PXR_DEBUG_NO_UPSCALE", 1)
 
     seed = 11
     w = bs.Workload(model, B, mode, seed=seed, grayscale=gray)

@@ -325,11 +325,16 @@ def fused_replay(torch, pkg, tag):
         np.testing.assert_array_equal(host["direction"], rec["final_direction"])
 
 
-@pytest.mark.parametrize("grid", [0, 3])
+@pytest.mark.parametrize("launch", ["one-per-cta", "grid3", "gather"])
 @pytest.mark.parametrize("tag", REPLAYS)
-def test_fused_replay_hash_chain(torch, pkg, knobs, tag, grid):
-    if grid:  # several envs per CTA
-        knobs.set("PXR_DEBUG_GRID", grid)
+def test_fused_replay_hash_chain(torch, pkg, knobs, tag, launch):
+    """The recorded reference chains through the fused step: one env per
+    CTA, several envs per CTA, and (video) the per-pixel texel gather
+    instead of the TMA copy of the upscaled frame."""
+    if launch == "grid3":  # several envs per CTA
+        knobs.set("PXR_DEBUG_GRID", 3)
+    elif launch == "gather":
+        knobs.set("PXR_DEBUG_NO_UPSCALE", 1)
     fused_replay(torch, pkg, tag)
 
 

@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(native):
 
 def test_abi_and_status_strings(native):
     lib = native.lib()
-    assert lib.pxr_abi_version() == 2
+    assert lib.pxr_abi_version() == 3
     assert lib.pxr_status_string(1) == b"invalid argument"
     if native.LIB_PATH.endswith("libpxr.so"):
         assert lib.pxr_build_checked() == 0  # the product build has no device checks
