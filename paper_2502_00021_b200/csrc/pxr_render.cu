@@ -163,6 +163,7 @@ struct RenderParams {
   // frame is TMA-copied into the colour buffer as its background
   const uint8_t *frames_hw;
   int hw;
+  int tris_smem;  // > 0: the triangle indices (u16) are staged in shared memory once per CTA
   uint32_t wmagic;  // ceil(2^32 / W): flat pixel index -> row
   int depth_vec;    // out_depth groups of 4 pixels are 16-byte aligned
   int band_h;       // rows per band: a frame is rendered in bands that fit shared memory
@@ -172,7 +173,7 @@ struct RenderParams {
 };
 
 struct SmemLayout {
-  int link, floor, maps, vxy64, viz, vxy32, vz, world, rows, ids, lrp, rec, span, rowner, queue,
+  int link, floor, maps, vxy64, viz, vxy32, vz, world, tris, rows, ids, lrp, rec, span, rowner, queue,
       frag, depth, col, wkey, gray, gplan, vframe, total;
 };
 
@@ -190,6 +191,7 @@ __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   L.vxy32 = o;  o += align_up(p.nv * 8, 16);
   L.vz = o;     o += align_up(p.nv * 4, 16);
   L.world = o;  o += align_up(p.nv * 12, 16);
+  L.tris = o;   o += p.tris_smem ? align_up(p.nt * 8, 16) : 0;  // u16 x 4 per triangle
   L.rows = o;   o += align_up((p.nt + 1) * 2, 16);  // bbox rows per triangle (0 = dead)
   L.ids = o;    o += align_up((p.nt + 1) * 2, 16);  // live index -> triangle
   L.lrp = o;    o += align_up((p.nt + 1) * 4, 16);  // live index -> bbox-row prefix
@@ -541,6 +543,7 @@ render_step_kernel(const RenderParams p) {
   float2 *s_vxy32 = reinterpret_cast<float2 *>(smem + L.vxy32);
   float *s_vz = reinterpret_cast<float *>(smem + L.vz);
   float *s_world = reinterpret_cast<float *>(smem + L.world);
+  uint2 *s_tris = reinterpret_cast<uint2 *>(smem + L.tris);  // (i0 | i1 << 16, i2)
   uint16_t *s_rows = reinterpret_cast<uint16_t *>(smem + L.rows);
   uint16_t *s_ids = reinterpret_cast<uint16_t *>(smem + L.ids);
   uint32_t *s_lrp = reinterpret_cast<uint32_t *>(smem + L.lrp);
@@ -587,6 +590,10 @@ render_step_kernel(const RenderParams p) {
       s_floor[p.W + p.H + i] = p.floor_rays[(int64_t)i * p.W * 3 + 2];
     }
   }
+  if (p.tris_smem && warp < kWarps - 1)  // the mesh's triangles, staged once per CTA
+    for (int t = tid; t < p.nt; t += kSetupThreads)
+      s_tris[t] = make_uint2((uint32_t)__ldg(p.tris + 3 * t) | ((uint32_t)__ldg(p.tris + 3 * t + 1) << 16),
+                             (uint32_t)__ldg(p.tris + 3 * t + 2));
   if (p.mode == PXR_MODE_VIDEO && warp < kWarps - 1) {  // nearest_map, distractor.py:179-181
     for (int i = tid; i < p.H; i += kSetupThreads)
       s_rowmap[i] = (uint32_t)(((int64_t)i * p.Hv) / p.H) * p.Wv * 3;
@@ -643,6 +650,20 @@ render_step_kernel(const RenderParams p) {
 
   __syncthreads();
   PXR_PROF(0);  // once per CTA: setup + the first env's preparation
+
+  // triangle t's vertex indices (shared memory, or L2 for meshes too large)
+  auto load_tri = [&](int t, int &a, int &b, int &c) {
+    if (p.tris_smem) {
+      const uint2 w = s_tris[t];
+      a = (int)(w.x & 0xffffu);
+      b = (int)(w.x >> 16);
+      c = (int)w.y;
+    } else {
+      a = __ldg(p.tris + 3 * t + 0);
+      b = __ldg(p.tris + 3 * t + 1);
+      c = __ldg(p.tris + 3 * t + 2);
+    }
+  };
 
   // liveness: each thread owns a contiguous block of triangles (index order)
   const int per = (p.nt + kThreads - 1) / kThreads;
@@ -735,11 +756,7 @@ render_step_kernel(const RenderParams p) {
     // so their latency (L2: the geometry does not stay in the small L1 next
     // to 230 KB of shared memory) overlaps it
     int n0 = 0, n1 = 0, n2 = 0;  // indices of the next triangle, loaded one ahead
-    if (t0 < t1) {
-      n0 = __ldg(p.tris + 3 * t0 + 0);
-      n1 = __ldg(p.tris + 3 * t0 + 1);
-      n2 = __ldg(p.tris + 3 * t0 + 2);
-    }
+    if (t0 < t1) load_tri(t0, n0, n1, n2);
 
     // ---- phase 1: world transform + projection (render.py:468-481, 350-363)
     vertex_phase(local_env);
@@ -800,19 +817,11 @@ render_step_kernel(const RenderParams p) {
       // each thread's block of triangles (t0, t1) is contiguous, so its live
       // count and bbox-row total feed the block scan directly
       int my_live = 0, my_rows = 0;
-      if (kBands && y0 > 0 && t0 < t1) {  // (the first band's were loaded at the env's start)
-        n0 = __ldg(p.tris + 3 * t0 + 0);
-        n1 = __ldg(p.tris + 3 * t0 + 1);
-        n2 = __ldg(p.tris + 3 * t0 + 2);
-      }
+      if (kBands && y0 > 0 && t0 < t1) load_tri(t0, n0, n1, n2);  // (band 0: at the env's start)
       for (int t = t0; t < t1; t++) {
         uint32_t rows = 0;
         const int i0 = n0, i1 = n1, i2 = n2;
-        if (t + 1 < t1) {
-          n0 = __ldg(p.tris + 3 * t + 3);
-          n1 = __ldg(p.tris + 3 * t + 4);
-          n2 = __ldg(p.tris + 3 * t + 5);
-        }
+        if (t + 1 < t1) load_tri(t + 1, n0, n1, n2);
         PXR_DCHECK(i0 >= 0 && i0 < p.nv && i1 >= 0 && i1 < p.nv && i2 >= 0 && i2 < p.nv);
         PXR_DCHECK(rows <= 0xFFFFu);
         const float z0 = s_vz[i0], z1 = s_vz[i1], z2 = s_vz[i2];
@@ -1073,8 +1082,8 @@ render_step_kernel(const RenderParams p) {
           // path branch they stalled the shading below by a full L2 latency
           const float tc0 = __ldg(p.tri_colors + 3 * t + 0), tc1 = __ldg(p.tri_colors + 3 * t + 1),
                       tc2 = __ldg(p.tri_colors + 3 * t + 2);
-          int i0 = __ldg(p.tris + 3 * t + 0), i1 = __ldg(p.tris + 3 * t + 1),
-              i2 = __ldg(p.tris + 3 * t + 2);
+          int i0, i1, i2;
+          load_tri(t, i0, i1, i2);
           const float2 a = s_vxy32[i0];
           float2 b = s_vxy32[i1], c = s_vxy32[i2];
           float area2 = (b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x);
@@ -1575,6 +1584,8 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   // Test hooks (tests/test_gpu_parity.py, pxr_set_debug): shrink the
   // per-round budgets so the multi-round and fragment-overflow paths run on
   // small inputs.
+  // meshes up to 2048 triangles keep their indices in shared memory (16 KB)
+  p.tris_smem = p.nt <= 2048 ? 1 : 0;
   p.frag_limit = kFragCap;
   p.row_cap = kRowCap > p.H ? kRowCap : p.H;
   {
