@@ -12,27 +12,35 @@
 // one env per CTA iteration, every intermediate in shared memory, every
 // phase a flat loop over the CTA:
 //   0. the env's video frame is fetched into shared memory by a TMA bulk
-//      copy (cp.async.bulk + mbarrier); its per-link glibc-exact cosf/sinf
-//      and distractor state (32 envs at a time, one lane per env) were
-//      prepared by one warp during the previous env's rasterisation;
+//      copy (cp.async.bulk + mbarrier) -- for RGB video with the pack
+//      upscaled to the frame size (pxr_pack_upscale) the upscaled frame is
+//      copied straight into the colour buffer instead, after phase 1; its
+//      per-link glibc-exact cosf/sinf and distractor state (32 envs at a
+//      time, one lane per env) were prepared by one warp during the
+//      previous env's rasterisation; the mesh's triangle indices sit in
+//      shared memory for the whole launch;
 //   1. world transform + projection of every vertex (f32 like the
 //      reference; f64 copies and 1/z for the raster);
 //   2. triangle liveness exactly as the reference culls (near/far, zero
 //      area, empty pixel bbox); a block scan over the triangles in index
 //      order gives live index + bbox-row prefix; the background (sky, floor,
-//      video texel) under an empty z-buffer, written as final colours (with
-//      the floor here, without it by the warps phase 3 leaves idle);
+//      video texel -- or, for the upscaled copy, only the empty z-buffer)
+//      written as final colours (with the floor here, without it by the
+//      warps phase 3 leaves idle);
 //   3. per round of live triangles (one round whenever the records fit): a
 //      record per triangle (edge vectors, exact reciprocal of the area, flat
 //      colour, the degenerate-normal cull) plus f32 line equations for
 //      conservative row spans; (triangle, bbox row) units in 32-row chunks
 //      dealt to the warps: each lane computes one row's conservative span,
-//      non-empty spans gather in a per-warp queue and every 32 are expanded
-//      into pixel candidates (warp scan + owner search), whole rounds of 32
-//      candidates at a time (the rest re-queued), for the reference's
-//      exact f64 edge / barycentric / depth arithmetic; covered fragments
-//      min-reduce their f32 depth per pixel with a 32-bit shared-memory
-//      atomicMin and are appended to a fragment list;
+//      non-empty spans gather in a per-warp queue; whenever 32 are queued
+//      each lane tests the first pixel of one span (a full round of 32
+//      candidates with no expansion) and re-queues the span's remaining
+//      pixels; at the end the queue is drained with a warp scan + owner
+//      search expanding the spans into whole rounds of candidates; every
+//      candidate gets the reference's exact f64 edge / barycentric / depth
+//      arithmetic; covered fragments min-reduce their f32 depth per pixel
+//      with a 32-bit shared-memory atomicMin and are appended to a fragment
+//      list;
 //   4. exact order-independent resolve of the reference's SEQUENTIAL strict
 //      z-test (render.py:452, triangles in index order, f64 z compared with
 //      the f32 z-buffer): with F = min over fragments of RN32(z) and
