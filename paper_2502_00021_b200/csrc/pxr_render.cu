@@ -1176,12 +1176,14 @@ render_step_kernel(const RenderParams p) {
         const int n_chunks = (n_rows + 31) >> 5;
         // while warp kWarps-1 prepares the next env the chunks are dealt to
         // the other warps only (it would otherwise finish last)
-        const int n_workers = prepared ? kWarps : kWarps - 1;
-        if (warp == kWarps - 1 && !prepared) {
+        // (`prepared` is the same in every thread: the chunk dealing below
+        // must be CTA-uniform, also in a second raster round)
+        const bool preparing = !prepared;
+        const int n_workers = preparing ? kWarps - 1 : kWarps;
+        if (warp == kWarps - 1 && preparing)
           prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
                       lane);
-          prepared = true;
-        }
+        prepared = true;
         uint2 *q = s_queue + warp * 64;
         // a covered candidate: min-reduce its f32 depth into the pixel and
         // take a fragment-list slot (ptxas aggregates the warp's increments
