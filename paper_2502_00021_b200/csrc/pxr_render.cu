@@ -130,6 +130,13 @@ constexpr int kQueue = 64;
 // live index of the round < 2^12 by the host's limits).
 constexpr int kMaxCap = 4095;
 
+// Shared-memory offsets of one CTA (smem_layout), computed on the host and
+// read from the kernel parameters: no registers, no recomputation.
+struct SmemLayout {
+  int link, floor, maps, vxy64, viz, vxy32, vz, world, tris, rows, ids, lrp, rec, span, rowner, queue,
+      frag, depth, col, wkey, gray, gplan, vframe, total;
+};
+
 struct RenderParams {
   const float *base_verts;
   const int32_t *vert_link;
@@ -178,12 +185,10 @@ struct RenderParams {
   int32_t *stats;   // debug (tools/render_stats.py): per env kStats workload counters, or null
   int scan_sh;      // > 0: live count << scan_sh | bbox rows fits 32 bits (one packed scan)
   long long *prof;  // debug (tools/phase_prof.py): per-CTA phase cycles, or null
+  SmemLayout L;     // set by the host from smem_layout(*this)
 };
 
-struct SmemLayout {
-  int link, floor, maps, vxy64, viz, vxy32, vz, world, tris, rows, ids, lrp, rec, span, rowner, queue,
-      frag, depth, col, wkey, gray, gplan, vframe, total;
-};
+
 
 __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
@@ -532,7 +537,7 @@ render_step_kernel(const RenderParams p) {
   __shared__ EnvShared es;
   __shared__ DistSlot s_dist[32];
   __shared__ int s_scan[2 * kWarps];
-  const SmemLayout L = smem_layout(p);
+  const SmemLayout &L = p.L;
 #ifdef PXR_CHECKED
   {
     uint32_t dyn;
@@ -1647,11 +1652,12 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     if (bh < height && (bh * bytes_row) % 16 != 0) p.use_bulk = 0;
     if (bh < height && (bh * width) % 4 != 0) p.depth_vec = 0;
   }
-  // RGB video, one band, the pack upscaled to this frame size: the env's
-  // background is one TMA copy of its upscaled frame (no texel gather, no
-  // raw-frame buffer in shared memory)
+  // RGB video without a drawn floor (the texel is the whole background), one
+  // band, the pack upscaled to this frame size: the env's background is one
+  // TMA copy of its upscaled frame (no texel gather, no raw-frame buffer in
+  // shared memory)
   p.hw = 0;
-  if (mode == PXR_MODE_VIDEO && p.band_h == p.H && !p.gray && p.use_bulk &&
+  if (mode == PXR_MODE_VIDEO && !p.draw_floor && p.band_h == p.H && !p.gray && p.use_bulk &&
       pack->frames_hw != nullptr && pack->hw_height == height && pack->hw_width == width &&
       (reinterpret_cast<uintptr_t>(pack->frames_hw) & 15) == 0 &&
       debug_knob(kDbgNoUpscale) == nullptr)
@@ -1667,7 +1673,8 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     while (lb < 32 && ((int64_t)1 << lb) <= (int64_t)p.nt) lb++;
     p.scan_sh = (rb + lb <= 32 && rb < 32 && debug_knob(kDbgNoPackedScan) == nullptr) ? rb : 0;
   }
-  const int smem = smem_layout(p).total;
+  p.L = smem_layout(p);
+  const int smem = p.L.total;
   if (smem > budget) return set_unsupported("frame too large for one CTA's shared memory");
   const bool banded = p.band_h < p.H;
   auto kernel = banded ? (p.draw_floor ? render_step_kernel<true, true>
