@@ -130,8 +130,7 @@ constexpr int kQueue = 64;
 // live index of the round < 2^12 by the host's limits).
 constexpr int kMaxCap = 4095;
 
-// Shared-memory offsets of one CTA (smem_layout), computed on the host and
-// read from the kernel parameters: no registers, no recomputation.
+// Shared-memory offsets of one CTA (smem_layout).
 struct SmemLayout {
   int link, floor, maps, vxy64, viz, vxy32, vz, world, tris, rows, ids, lrp, rec, span, rowner, queue,
       frag, depth, col, wkey, gray, gplan, vframe, total;
@@ -185,7 +184,6 @@ struct RenderParams {
   int32_t *stats;   // debug (tools/render_stats.py): per env kStats workload counters, or null
   int scan_sh;      // > 0: live count << scan_sh | bbox rows fits 32 bits (one packed scan)
   long long *prof;  // debug (tools/phase_prof.py): per-CTA phase cycles, or null
-  SmemLayout L;     // set by the host from smem_layout(*this)
 };
 
 
@@ -537,7 +535,7 @@ render_step_kernel(const RenderParams p) {
   __shared__ EnvShared es;
   __shared__ DistSlot s_dist[32];
   __shared__ int s_scan[2 * kWarps];
-  const SmemLayout &L = p.L;
+  const SmemLayout L = smem_layout(p);
 #ifdef PXR_CHECKED
   {
     uint32_t dyn;
@@ -1673,8 +1671,7 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
     while (lb < 32 && ((int64_t)1 << lb) <= (int64_t)p.nt) lb++;
     p.scan_sh = (rb + lb <= 32 && rb < 32 && debug_knob(kDbgNoPackedScan) == nullptr) ? rb : 0;
   }
-  p.L = smem_layout(p);
-  const int smem = p.L.total;
+  const int smem = smem_layout(p).total;
   if (smem > budget) return set_unsupported("frame too large for one CTA's shared memory");
   const bool banded = p.band_h < p.H;
   auto kernel = banded ? (p.draw_floor ? render_step_kernel<true, true>
