@@ -487,15 +487,68 @@ def render(meshes, camera: Camera, light_dir=LIGHT_DIR, width: int = 84, height:
 def render_batch(scenes, width: int = 84, height: int = 84, floor_in_background: bool = False,
                  light_dir=LIGHT_DIR) -> Frame:
     """render.py:536-552: independent scenes, scene i bit-identical to
-    ``render(scene i)``; one launch per scene into its slice of the batch."""
+    ``render(scene i)``. The reference renders the batch on a thread pool;
+    here every scene's world-space mesh goes up in one upload, each scene
+    is one single-CTA launch (its own camera, floor-ray table and mesh), and
+    the launches are spread over several CUDA streams so the scenes render
+    concurrently on different SMs."""
+    import torch
+
     scenes = list(scenes)
     if not scenes:
         raise ValueError("render_batch needs at least one scene")
     if width < 8 or height < 8:
         raise ValueError("render needs width, height >= 8")
+    W, H = int(width), int(height)
     dev = _native.require_cuda()
-    frame = Frame.allocate(len(scenes), int(height), int(width), device=dev)
+    frame = Frame.allocate(len(scenes), H, W, device=dev)
+    light = np.asarray(light_dir, dtype=np.float32)
+    worlds = [_scene_world(list(meshes)) for meshes, _ in scenes]
+    for verts, tris, _ in worlds:
+        if len(verts) > 65535 or len(tris) > 65535:
+            raise ValueError("scene too large for the raster kernel (max 65535 vertices / triangles)")
+    nvs = [len(w[0]) for w in worlds]
+    nts = [len(w[1]) for w in worlds]
+    voff = np.concatenate([[0], np.cumsum(nvs)]).astype(np.int64)
+    toff = np.concatenate([[0], np.cumsum(nts)]).astype(np.int64)
+    # one upload for the whole batch (each scene's geometry points into it)
+    verts = torch.from_numpy(np.concatenate([w[0] for w in worlds]).reshape(-1, 3)
+                             if voff[-1] else np.zeros((1, 3), np.float32)).to(dev)
+    tris = torch.from_numpy(np.concatenate([w[1] for w in worlds]).reshape(-1, 3)
+                            if toff[-1] else np.zeros((1, 3), np.int32)).to(dev)
+    cols = torch.from_numpy(np.concatenate([w[2] for w in worlds]).reshape(-1, 3)
+                            if toff[-1] else np.zeros((1, 3), np.float32)).to(dev)
+    links = torch.zeros(max(1, int(voff[-1])), dtype=torch.int32, device=dev)
+    pose = torch.zeros((1, 1, 3), dtype=torch.float64, device=dev)
+    rays = torch.empty((len(scenes), H, W, 3), dtype=torch.float64, device=dev)
+    L = _native.lib()
+    main = torch.cuda.current_stream(dev)
+    streams = [torch.cuda.Stream(device=dev) for _ in range(min(len(scenes), 8))]
+    for s in streams:
+        s.wait_stream(main)  # (the uploads above)
+    keep = []
+    dist_c = _native.Distractor(_native.MODE_NONE)
     for i, (meshes, camera) in enumerate(scenes):
-        _render_scene_into(list(meshes), camera, light_dir, int(width), int(height),
-                           floor_in_background, frame.pixels[i:i + 1], frame.depth[i:i + 1], dev)
+        st = _native.stream_ptr(streams[i % len(streams)])
+        blk_np = camera_basis(camera)
+        blk = (ctypes.c_float * 15)(*blk_np.tolist())
+        sep = ctypes.c_int32(0)
+        _native.check(L.pxr_floor_rays(blk, H, W, rays[i].data_ptr(), ctypes.byref(sep), st))
+        geom_c = _native.Geometry(verts[int(voff[i]):].data_ptr(), links.data_ptr(),
+                                  tris[int(toff[i]):].data_ptr(), cols[int(toff[i]):].data_ptr(),
+                                  nvs[i], nts[i], 1)
+        cam_c = _native.Camera(blk, float(blk_np[0]), float(blk_np[2]),
+                               (ctypes.c_float * 3)(*light.tolist()), rays[i].data_ptr(),
+                               int(sep.value))
+        keep.append((blk, geom_c, cam_c))
+        _native.check(L.pxr_render_step(
+            ctypes.byref(geom_c), ctypes.byref(cam_c), pose.data_ptr(), 1, H, W,
+            int(not floor_in_background), ctypes.byref(dist_c), None, 0, None, None, 0,
+            frame.pixels[i:i + 1].data_ptr(), frame.depth[i:i + 1].data_ptr(), st))
+    for s in streams:
+        main.wait_stream(s)
+    # the uploads and tables are in use on the side streams until they finish
+    for t in (verts, tris, cols, links, pose, rays):
+        for s in streams:
+            t.record_stream(s)
     return frame
