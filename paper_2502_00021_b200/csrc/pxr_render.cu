@@ -398,11 +398,19 @@ __device__ __forceinline__ float3 world_vertex(const RenderParams &p, const floa
   return make_float3(lk.x + bx * lk.z - bz * lk.w, by, lk.y + bx * lk.w + bz * lk.z);
 }
 
+// Inclusive warp scan: shfl.up's own in-range predicate selects the add (no
+// separate lane compare per step).
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 #pragma unroll
   for (int s = 1; s < 32; s <<= 1) {
-    const int u = __shfl_up_sync(kFull, v, s);
-    if (lane >= s) v += u;
+    asm("{\n"
+        ".reg .s32 u;\n"
+        ".reg .pred p;\n"
+        "shfl.sync.up.b32 u|p, %0, %1, 0, -1;\n"
+        "@p add.s32 %0, %0, u;\n"
+        "}\n"
+        : "+r"(v)
+        : "r"(s));
   }
   return v;
 }
