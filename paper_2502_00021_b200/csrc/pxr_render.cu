@@ -335,23 +335,14 @@ __device__ __forceinline__ void floor_px(const RenderParams &p, float ex, float 
 // int(ceil(mn - 0.5)) .. int(floor(mx - 0.5)), lower end clamped to 0 and
 // upper end to lim (so lo > hi means empty). f64 in the reference; for
 // |v| < 2^21 the f32 value v - 0.5 is exact, so f32 ceil/floor give the same
-// integers without f64 conversions.
+// integers without f64 conversions. For |v| >= 2^21 the f32 value keeps its
+// sign and lies far outside [0, lim], which is all the clamped range depends
+// on (a bound beyond either end clamps or empties the range exactly as the
+// f64 one does; float -> int conversion saturates). Branch-free, so the x
+// and y sides of a triangle overlap.
 __device__ __forceinline__ void pixel_range(float mn, float mx, int lim, int &lo, int &hi) {
-  if (fabsf(mn) < 0x1p21f && fabsf(mx) < 0x1p21f) {
-    lo = (int)fmaxf(ceilf(mn - 0.5f), 0.0f);
-    hi = (int)fminf(floorf(mx - 0.5f), (float)lim);
-  } else {
-    double a = ceil((double)mn - 0.5), b = floor((double)mx - 0.5);
-    if (a < 0.0) a = 0.0;
-    if (b > (double)lim) b = (double)lim;
-    if (a > b) {  // empty; keep the integers in range
-      lo = 1;
-      hi = 0;
-    } else {
-      lo = (int)a;
-      hi = (int)b;
-    }
-  }
+  lo = (int)fmaxf(ceilf(mn - 0.5f), 0.0f);
+  hi = (int)fminf(floorf(mx - 0.5f), (float)lim);
 }
 
 // World-space vertex v (render.py:470-481): f32, no FMA contraction.
