@@ -56,6 +56,7 @@ enum DebugKnob {
   kDbgGrid,          // PXR_DEBUG_GRID: at most this many CTAs (several envs per CTA)
   kDbgProf,          // PXR_DEBUG_PROF: device int64 (grid, 12) per-CTA phase cycles
   kDbgNoUpscale,     // PXR_DEBUG_NO_UPSCALE: gather video texels even with an upscaled pack
+  kDbgNoPdl,         // PXR_DEBUG_NO_PDL: launch the render kernel without programmatic dependent launch
   kDbgCount
 };
 // value of a knob, or nullptr when unset
@@ -81,6 +82,14 @@ inline pxr_status check_launch(const char *where) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda(e, where);
   return PXR_OK;
+}
+
+// Programmatic dependent launch trigger: a kernel that may precede the
+// render launch lets it be scheduled early (its CTAs then wait in
+// griddepcontrol.wait for this grid to complete and flush, so the trigger's
+// position does not matter for correctness). No-op without a PDL dependent.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // ---- TMA bulk (non-tensor) copies, shared::cta -> global -----------------

@@ -42,7 +42,8 @@ pxr_status set_cuda(cudaError_t e, const char *where) {
 static const char *const kKnobNames[kDbgCount] = {
     "PXR_DEBUG_FRAG_LIMIT", "PXR_DEBUG_ROW_CAP",        "PXR_DEBUG_CAP",  "PXR_DEBUG_STATS_PTR",
     "PXR_DEBUG_BAND_H",     "PXR_DEBUG_NO_PACKED_SCAN", "PXR_DEBUG_PHYS", "PXR_DEBUG_GRID",
-    "PXR_DEBUG_PROF",       "PXR_DEBUG_NO_UPSCALE"};
+    "PXR_DEBUG_PROF",       "PXR_DEBUG_NO_UPSCALE",
+    "PXR_DEBUG_NO_PDL"};
 static std::mutex g_knob_mu;
 static std::string g_knob_val[kDbgCount];
 static bool g_knob_set[kDbgCount];
@@ -271,6 +272,7 @@ __device__ __forceinline__ void fk_one(const double *q, const int32_t *parent,
 
 __global__ void fk_kernel(const double *qpos, const int32_t *parent, const double *adist,
                           int nl, int64_t batch, double *poses) {
+  pdl_trigger();  // the render launch that follows may be scheduled now
   const int dof = 3 + nl - 1;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch;
        b += (int64_t)gridDim.x * blockDim.x)
@@ -285,6 +287,7 @@ __global__ void pose_source_kernel(const double *rest, const int32_t *parent,
                                    const double *adist, int nl, uint64_t rhi, uint64_t rlo,
                                    uint64_t env_offset, int64_t t, int64_t batch,
                                    double *poses) {
+  pdl_trigger();  // the render launch that follows may be scheduled now
   constexpr int kMaxDof = 3 + 63;
   const int dof = 3 + nl - 1;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch;

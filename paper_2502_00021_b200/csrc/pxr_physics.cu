@@ -621,6 +621,7 @@ __global__ void reset_kernel(const double *rest, int nd, double *qpos, double *q
 // physics.py:114-137 (same kernel as pxr_forward_kinematics, own copy here)
 __global__ void fk_env_kernel(const double *qpos, const int32_t *parent, const double *adist,
                               int nl, int64_t batch, double *poses) {
+  pdl_trigger();  // the render launch that follows may be scheduled now
   const int dof = 3 + nl - 1;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch;
        b += (int64_t)gridDim.x * blockDim.x) {

@@ -542,6 +542,14 @@ render_step_kernel(const RenderParams p) {
     PXR_DCHECK((uint32_t)L.total <= dyn);
   }
 #endif
+  // Programmatic dependent launch: the next launch in the stream may be
+  // scheduled now (its CTAs take SMs as this grid's CTAs exit), and this
+  // grid waits here for the previous one to complete and flush -- every
+  // global read below (poses, distractor state, geometry, floor rays) comes
+  // after the wait, so the overlap is the launch latency and CTA start-up
+  // only. Both are no-ops for a launch without the attribute.
+  pdl_trigger();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   float4 *s_link = reinterpret_cast<float4 *>(smem + L.link);
   double *s_floor = reinterpret_cast<double *>(smem + L.floor);  // dx[W], dy[H], dz[H]
   double *s_ft = s_floor + p.W + 2 * p.H;                          // per-row floor t
@@ -1683,6 +1691,26 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   int64_t grid = (int64_t)dev.num_sms * per_sm;
   if (debug_grid > 0 && debug_grid < grid) grid = debug_grid;
   if (grid > batch) grid = batch;
-  kernel<<<(unsigned)grid, kThreads, smem, st>>>(p);
+  if (debug_knob(kDbgNoPdl) != nullptr) {
+    kernel<<<(unsigned)grid, kThreads, smem, st>>>(p);
+    return check_launch("render_step_kernel");
+  }
+  // programmatic dependent launch (see the kernel's first lines): the launch
+  // latency of back-to-back steps overlaps the previous step's tail
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t le = cudaLaunchKernelEx(&cfg, kernel, p);
+  if (le != cudaSuccess) {
+    (void)cudaGetLastError();
+    return set_cuda(le, "render_step_kernel");
+  }
   return check_launch("render_step_kernel");
 }
