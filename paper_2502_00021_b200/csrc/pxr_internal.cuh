@@ -57,6 +57,7 @@ enum DebugKnob {
   kDbgProf,          // PXR_DEBUG_PROF: device int64 (grid, 12) per-CTA phase cycles
   kDbgNoUpscale,     // PXR_DEBUG_NO_UPSCALE: gather video texels even with an upscaled pack
   kDbgNoPdl,         // PXR_DEBUG_NO_PDL: launch the render kernel without programmatic dependent launch
+  kDbgNoSplit,       // PXR_DEBUG_NO_SPLIT: small batches keep one CTA per env
   kDbgCount
 };
 // value of a knob, or nullptr when unset

@@ -43,7 +43,7 @@ static const char *const kKnobNames[kDbgCount] = {
     "PXR_DEBUG_FRAG_LIMIT", "PXR_DEBUG_ROW_CAP",        "PXR_DEBUG_CAP",  "PXR_DEBUG_STATS_PTR",
     "PXR_DEBUG_BAND_H",     "PXR_DEBUG_NO_PACKED_SCAN", "PXR_DEBUG_PHYS", "PXR_DEBUG_GRID",
     "PXR_DEBUG_PROF",       "PXR_DEBUG_NO_UPSCALE",
-    "PXR_DEBUG_NO_PDL"};
+    "PXR_DEBUG_NO_PDL",     "PXR_DEBUG_NO_SPLIT"};
 static std::mutex g_knob_mu;
 static std::string g_knob_val[kDbgCount];
 static bool g_knob_set[kDbgCount];

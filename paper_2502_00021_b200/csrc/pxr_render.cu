@@ -64,6 +64,8 @@
 // (__fma_rn / __fmaf_rn): the glibc sinf/cosf restatement, the exact
 // division below and the conservative span bounds (not compared bit-wise).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -129,6 +131,8 @@ constexpr int kQueue = 64;
 // (depths are positive, so the f32 sign bit is free; pix < 2^20 and the
 // live index of the round < 2^12 by the host's limits).
 constexpr int kMaxCap = 4095;
+// Small batches: an env is split over CTAs in bands of at least this many rows.
+constexpr int kMinSplitRows = 12;
 
 // Shared-memory offsets of one CTA (smem_layout).
 struct SmemLayout {
@@ -184,6 +188,12 @@ struct RenderParams {
   int32_t *stats;   // debug (tools/render_stats.py): per env kStats workload counters, or null
   int scan_sh;      // > 0: live count << scan_sh | bbox rows fits 32 bits (one packed scan)
   long long *prof;  // debug (tools/phase_prof.py): per-CTA phase cycles, or null
+  // Small batches: `split` CTAs render one env, one row band each (no
+  // cross-CTA communication: only launched when no band reads distractor
+  // state another band writes); 1 = persistent CTAs, each a sequence of
+  // whole envs.
+  int split;
+  int64_t env_stride;  // envs between a CTA's consecutive envs (= gridDim.x / split)
 };
 
 
@@ -250,7 +260,7 @@ struct EnvShared {
 //           reset the re-drawn video (env.py:226-244); frame index 204.
 // With advance == 0 (make_env / observe) the stored state is used as is.
 __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t env,
-                                                  DistSlot &out) {
+                                                  DistSlot &out, bool write) {
   const uint64_t g = p.env_offset + (uint64_t)env;
   out.bias[0] = out.bias[1] = out.bias[2] = 0;
   out.frame_idx = 0;
@@ -262,7 +272,8 @@ __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t
       uint64_t ehi, elo;
       threefry2x64(key_hi, key_lo, g, 2, ehi, elo);
       color_bias_from_key(ehi, elo, b3);
-      for (int c = 0; c < 3; c++) p.color_bias[env * 3 + c] = b3[c];
+      if (write)  // (split env: band 0 only; the new bias does not read the old)
+        for (int c = 0; c < 3; c++) p.color_bias[env * 3 + c] = b3[c];
     } else {
       for (int c = 0; c < 3; c++) b3[c] = p.color_bias[env * 3 + c];
     }
@@ -270,7 +281,7 @@ __device__ __forceinline__ void distractor_update(const RenderParams &p, int64_t
   } else if (p.mode == PXR_MODE_VIDEO) {
     int64_t vid = p.video_index[env];
     int64_t cur = p.frame_cursor[env];
-    if (p.advance) {
+    if (p.advance) {  // (never split: the step reads the state it writes)
       int dir = p.direction[env];
       const int64_t cnt = p.frame_count[env];
       int64_t nxt = cur + dir;
@@ -354,7 +365,7 @@ __device__ __forceinline__ void pixel_range(float mn, float mx, int lim, int &lo
 // envs of this CTA is advanced at once, one lane each.
 __device__ __forceinline__ void prepare_env(const RenderParams &p, int64_t env, int local_env,
                                          float4 *link_buf, DistSlot *s_dist, EnvShared &es,
-                                         int lane) {
+                                         int lane, int64_t stride, bool write) {
   for (int l = lane; l < p.nl; l += 32) {
     const double *pp = p.poses + (env * p.nl + l) * 3;
     const float th = (float)pp[2];  // poses.astype(float32), render.py:613
@@ -362,8 +373,8 @@ __device__ __forceinline__ void prepare_env(const RenderParams &p, int64_t env, 
                               glibc_sincosf(th, 0));
   }
   if (local_env % 32 == 0) {
-    const int64_t e2 = env + (int64_t)lane * gridDim.x;
-    if (e2 < p.batch) distractor_update(p, e2, s_dist[lane]);
+    const int64_t e2 = env + (int64_t)lane * stride;
+    if (e2 < p.batch) distractor_update(p, e2, s_dist[lane], write);
   }
   __syncwarp();
   if (lane == 0) {
@@ -599,8 +610,15 @@ render_step_kernel(const RenderParams p) {
   // warp prepares the first env (its latency chain would otherwise open the
   // CTA's critical path: a whole launch at small batches) ------------------
   constexpr int kSetupThreads = kThreads - 32;  // every warp but the last
-  if (warp == kWarps - 1 && blockIdx.x < p.batch)
-    prepare_env(p, blockIdx.x, 0, s_link, s_dist, es, lane);
+  // split env: this CTA renders band `band0` of env blockIdx.x / split
+  const int band0 = kBands && p.split > 1 ? (int)(blockIdx.x % (unsigned)p.split) : 0;
+  const int64_t env_first =
+      kBands && p.split > 1 ? (int64_t)(blockIdx.x / (unsigned)p.split) : (int64_t)blockIdx.x;
+  // envs between this CTA's consecutive envs (the grid without a split)
+  const int64_t env_stride = kBands ? p.env_stride : (int64_t)gridDim.x;
+  const bool dist_write = !kBands || band0 == 0;  // a split env's state: band 0 writes
+  if (warp == kWarps - 1 && env_first < p.batch)
+    prepare_env(p, env_first, 0, s_link, s_dist, es, lane, env_stride, dist_write);
   if (kFloor && p.floor_sep && warp < kWarps - 1) {
     for (int i = tid; i < p.W; i += kSetupThreads) s_floor[i] = p.floor_rays[(int64_t)i * 3];
     for (int i = tid; i < p.H; i += kSetupThreads) {
@@ -756,7 +774,7 @@ render_step_kernel(const RenderParams p) {
 
   uint32_t vphase = 0;
   int local_env = 0;
-  for (int64_t env = blockIdx.x; env < p.batch; env += gridDim.x, local_env++) {
+  for (int64_t env = env_first; env < p.batch; env += env_stride, local_env++) {
     // ---- phase 0: video fetch (the env's link trig, camera and distractor
     // state were prepared by warp kWarps-1 during the previous env) -------
     const int cb = local_env & 1;
@@ -768,7 +786,7 @@ render_step_kernel(const RenderParams p) {
                     (uint32_t)p.vframe_bytes, &es.vbar);
     }
     const float ex = es.ex[cb], ez = es.ez[cb];
-    bool prepared = env + gridDim.x >= p.batch;  // nothing to prepare for a last env
+    bool prepared = env + env_stride >= p.batch;  // nothing to prepare for a last env
 
     // the first liveness triangle's indices, loaded before the vertex phase
     // so their latency (L2: the geometry does not stay in the small L1 next
@@ -786,7 +804,8 @@ render_step_kernel(const RenderParams p) {
     // ---- bands of rows: everything below runs once per band (one band
     // whenever the frame's per-pixel state fits shared memory) ------------
     const int band_h = kBands ? p.band_h : p.H;
-    int yb = 0;
+    const int ystart = kBands ? band0 * band_h : 0;  // a split env: this CTA's band only
+    int yb = ystart;
     do {  // (no loop at all for one band)
       const int y0 = kBands ? yb : 0;  // compile-time 0 for one band
       const int y1 = kBands ? min(y0 + band_h, p.H) : p.H;
@@ -826,7 +845,7 @@ render_step_kernel(const RenderParams p) {
         bulk_load_g2s(s_col, p.frames_hw + es.frame_idx[cb] * p.frame_bytes,
                       (uint32_t)p.frame_bytes, &es.vbar);
       }
-      if (kBands && y0 > 0) {  // the previous band's TMA store must have finished reading
+      if (kBands && y0 > ystart) {  // the previous band's TMA store must have finished reading
         if (tid == 0 && p.use_bulk) bulk_wait_read();
         __syncthreads();
       }
@@ -835,7 +854,7 @@ render_step_kernel(const RenderParams p) {
       // each thread's block of triangles (t0, t1) is contiguous, so its live
       // count and bbox-row total feed the block scan directly
       int my_live = 0, my_rows = 0;
-      if (kBands && y0 > 0 && t0 < t1) load_tri(t0, n0, n1, n2);  // (band 0: at the env's start)
+      if (kBands && y0 > ystart && t0 < t1) load_tri(t0, n0, n1, n2);  // (first band: at the env's start)
       for (int t = t0; t < t1; t++) {
         uint32_t rows = 0;
         const int i0 = n0, i1 = n1, i2 = n2;
@@ -872,9 +891,9 @@ render_step_kernel(const RenderParams p) {
       // a floor (cheap texel / sky pixels) it is written by the warps the
       // records phase leaves idle (see below), else here by every thread:
       // threads first, first + stride, ...
-      const bool vwait = y0 == 0 && p.mode == PXR_MODE_VIDEO && !p.hw && p.vframe_bulk;
+      const bool vwait = y0 == ystart && p.mode == PXR_MODE_VIDEO && !p.hw && p.vframe_bulk;
       const uint32_t vpar = vphase;
-      if (y0 == 0) vphase ^= 1u;  // the env's video frame (one fetch for all bands)
+      if (y0 == ystart) vphase ^= 1u;  // the env's video frame (one fetch for all bands)
       auto background = [&](int first, int stride) {
         if (!kBands && p.hw) {  // colours arrive by TMA: depth +inf, empty keys
           const float inf = __int_as_float(0x7f800000);
@@ -1191,8 +1210,8 @@ render_step_kernel(const RenderParams p) {
         const bool preparing = !prepared;
         const int n_workers = preparing ? kWarps - 1 : kWarps;
         if (warp == kWarps - 1 && preparing)
-          prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
-                      lane);
+          prepare_env(p, env + env_stride, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
+                      lane, env_stride, dist_write);
         prepared = true;
         uint2 *q = s_queue + warp * 64;
         // a covered candidate: min-reduce its f32 depth into the pixel and
@@ -1398,7 +1417,8 @@ render_step_kernel(const RenderParams p) {
         r0 = r1;
       }
       if (warp == kWarps - 1 && !prepared)  // env without live triangles
-        prepare_env(p, env + gridDim.x, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es, lane);
+        prepare_env(p, env + env_stride, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es, lane,
+                    env_stride, dist_write);
 
       // ---- depth output (debug / _render_frame parity only) ---------------
       if (p.out_depth != nullptr) {
@@ -1428,7 +1448,7 @@ render_step_kernel(const RenderParams p) {
         __syncthreads();
       }
       yb += band_h;
-    } while (kBands && yb < p.H);
+    } while (kBands && p.split == 1 && yb < p.H);
   }
   // the last frame store must have read shared memory before the CTA exits
   // (its global writes complete with the grid)
@@ -1653,6 +1673,26 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
       if (smem_layout(p).total <= budget) break;
     }
     if (debug_band > 0 && debug_band < bh) bh = debug_band;
+    // Small batches (at most half as many envs as SMs): each env is split
+    // over CTAs, one band of >= kMinSplitRows rows each, so the per-band
+    // phases (records, raster, resolve, paint) run on several SMs at once.
+    // No CTA communicates with another: only when no band reads distractor
+    // state another band writes (video with advance reads and writes the
+    // ping-pong cursor; the colour step re-draws the bias from the key and
+    // band 0 alone writes it back).
+    p.split = 1;
+    if (bh == height && !(mode == PXR_MODE_VIDEO && advance) && debug_grid <= 0 &&
+        debug_knob(kDbgNoSplit) == nullptr && batch * 2 <= dev.num_sms) {
+      const int64_t want = std::min<int64_t>(dev.num_sms / batch, height / kMinSplitRows);
+      if (want >= 2) {
+        int sb = (int)((height + want - 1) / want);
+        sb = (sb + m - 1) / m * m;  // whole 16-byte multiples
+        if (sb < height) {
+          bh = sb;
+          p.split = (int)((height + sb - 1) / sb);
+        }
+      }
+    }
     p.band_h = bh;
     if (bh < height && (bh * bytes_row) % 16 != 0) p.use_bulk = 0;
     if (bh < height && (bh * width) % 4 != 0) p.depth_vec = 0;
@@ -1691,6 +1731,8 @@ extern "C" pxr_status pxr_render_step(const pxr_geometry *geom, const pxr_camera
   int64_t grid = (int64_t)dev.num_sms * per_sm;
   if (debug_grid > 0 && debug_grid < grid) grid = debug_grid;
   if (grid > batch) grid = batch;
+  if (p.split > 1) grid = batch * p.split;  // (<= the SM count, host rule above)
+  p.env_stride = grid / p.split;
   if (debug_knob(kDbgNoPdl) != nullptr) {
     kernel<<<(unsigned)grid, kThreads, smem, st>>>(p);
     return check_launch("render_step_kernel");
