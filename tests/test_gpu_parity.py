@@ -116,16 +116,29 @@ class TestDeviceMath:
         assert (int(hi.cpu()[0]), int(lo.cpu()[0])) == (0x68E3DF91C05D6C14, 0x741BFF0A50063A5F)
 
 
+def set_launch(knobs, launch):
+    """split: the default small-batch launch (each env split over CTAs, one
+    row band each); one-per-cta: one CTA per env; grid3: at most 3 CTAs, so
+    every CTA renders several envs."""
+    if launch == "one-per-cta":
+        knobs.set("PXR_DEBUG_NO_SPLIT", 1)
+    elif launch == "grid3":
+        knobs.set("PXR_DEBUG_GRID", 3)
+
+
+LAUNCHES = ["split", "one-per-cta", "grid3"]
+
+
 class TestRenderGolden:
-    @pytest.mark.parametrize("grid", [0, 3])
+    @pytest.mark.parametrize("launch", LAUNCHES)
     @pytest.mark.parametrize("name", MODEL_NAMES)
-    def test_frames_exact(self, torch, pkg, knobs, name, grid):
-        """Golden frames with one env per CTA, and with at most 3 CTAs (every
-        CTA renders several envs: the cross-env prefetch of link trig and
-        distractor slot, the double-buffered link table, the video mbarrier
-        parity flip, the TMA store overlapping the next env)."""
-        if grid:
-            knobs.set("PXR_DEBUG_GRID", grid)
+    def test_frames_exact(self, torch, pkg, knobs, name, launch):
+        """Golden frames with each env split over CTAs (the small-batch
+        default), one env per CTA, and at most 3 CTAs (every CTA renders
+        several envs: the cross-env prefetch of link trig and distractor
+        slot, the double-buffered link table, the video mbarrier parity flip,
+        the TMA store overlapping the next env)."""
+        set_launch(knobs, launch)
         rec = golden(f"render_{name}.npz")
         geom = geometry_of(name)
         poses = to_dev(torch, rec["poses"])
@@ -148,13 +161,12 @@ class TestRenderGolden:
         {"PXR_DEBUG_BAND_H": "7", "PXR_DEBUG_CAP": "40"},  # bands + rounds, plain stores
         {"PXR_DEBUG_NO_PACKED_SCAN": "1", "PXR_DEBUG_CAP": "40"},  # two-scan block scan
     ])
-    @pytest.mark.parametrize("grid", [0, 3])
-    def test_round_and_overflow_paths_exact(self, torch, pkg, knobs, kv, grid):
+    @pytest.mark.parametrize("launch", LAUNCHES)
+    def test_round_and_overflow_paths_exact(self, torch, pkg, knobs, kv, launch):
         """The multi-round and fragment-overflow paths (only reached by large
-        meshes / frames at default budgets) forced on the golden frames; also
-        with at most 3 CTAs (several envs per CTA)."""
-        if grid:
-            knobs.set("PXR_DEBUG_GRID", grid)
+        meshes / frames at default budgets) forced on the golden frames, with
+        each launch shape."""
+        set_launch(knobs, launch)
         for k, v in kv.items():
             knobs.set(k, v)
         for name in ("humanoid_lite", "cheetah_lite"):
@@ -325,17 +337,50 @@ def fused_replay(torch, pkg, tag):
         np.testing.assert_array_equal(host["direction"], rec["final_direction"])
 
 
-@pytest.mark.parametrize("launch", ["one-per-cta", "grid3", "gather"])
+@pytest.mark.parametrize("launch", LAUNCHES + ["gather"])
 @pytest.mark.parametrize("tag", REPLAYS)
 def test_fused_replay_hash_chain(torch, pkg, knobs, tag, launch):
-    """The recorded reference chains through the fused step: one env per
-    CTA, several envs per CTA, and (video) the per-pixel texel gather
-    instead of the TMA copy of the upscaled frame."""
-    if launch == "grid3":  # several envs per CTA
-        knobs.set("PXR_DEBUG_GRID", 3)
-    elif launch == "gather":
+    """The recorded reference chains through the fused step: the default
+    launch (colour / none: each env split over CTAs), one env per CTA,
+    several envs per CTA, and (video) the per-pixel texel gather instead of
+    the TMA copy of the upscaled frame."""
+    if launch == "gather":
         knobs.set("PXR_DEBUG_NO_UPSCALE", 1)
+    else:
+        set_launch(knobs, launch)
     fused_replay(torch, pkg, tag)
+
+
+@pytest.mark.parametrize("mode", ["none", "color", "video"])
+@pytest.mark.parametrize("B", [1, 21, 37, 60])
+def test_split_launch_equals_one_cta_per_env(torch, pkg, knobs, mode, B):
+    """Small batches render each env on several CTAs (one row band each):
+    frames, depth and the distractor state after several advancing steps
+    with resets equal the one-CTA-per-env launch byte for byte (video
+    advances never split; its make_env / observe render does)."""
+    from paper_2502_00021_b200 import bench_support as bs
+
+    outs = []
+    for no_split in (False, True):
+        knobs.set("PXR_DEBUG_NO_SPLIT", 1 if no_split else None)
+        w = bs.Workload("ant_lite", B, mode, seed=11)
+        frames = []
+        for t in range(4):
+            poses = w.poses(t)
+            done = torch.zeros(B, dtype=torch.uint8, device=poses.device)
+            done[t % B] = 1
+            obs, depth = w.render(poses, t, advance=t > 0, want_depth=True,
+                                  done=done if t > 0 else None)
+            frames.append((obs.clone(), depth.clone()))
+        torch.cuda.synchronize()
+        state = w.dist.to_host() if mode != "none" else {}
+        outs.append((frames, state))
+    (fa, sa), (fb, sb) = outs
+    for (oa, da), (ob, db) in zip(fa, fb):
+        assert torch.equal(oa, ob)
+        assert torch.equal(da.view(torch.int32), db.view(torch.int32))
+    for k in sa:
+        np.testing.assert_array_equal(sa[k], sb[k])
 
 
 @pytest.mark.parametrize("tag,band", [("walker_video_b8", "12"), ("hopper_color_gray_b4", "5"),
