@@ -1186,6 +1186,8 @@ render_step_kernel(const RenderParams p) {
           s_span[li - r0] = S;
           const uint32_t u1 = u0 + (uint32_t)(by1 - by0 + 1);
           PXR_DCHECK(((u1 - 1) >> 5) < (uint32_t)(p.row_cap / 32 + 2));
+          // (mostly 0 or 1 chunk starts: no unrolled remainder dispatch)
+#pragma unroll 1
           for (uint32_t k = (u0 + 31) >> 5; k <= ((u1 - 1) >> 5); k++)
             s_rowner[k] = (uint16_t)(li - r0);
         }
@@ -1359,6 +1361,8 @@ render_step_kernel(const RenderParams p) {
           __syncthreads();
         }
         if (n_frag <= p.frag_limit) {
+          // (at most kFragCap / kThreads = 2 iterations: not unrolled)
+#pragma unroll 1
           for (int i = tid; i < n_frag; i += kThreads) {
             const uint2 f = s_frag[i];
             const uint32_t pix = f.y & 0xFFFFFu, tri = f.y >> 20;
@@ -1370,12 +1374,14 @@ render_step_kernel(const RenderParams p) {
           }
           __syncthreads();
           PXR_PROF(5);  // resolve pass
+#pragma unroll 1
           for (int i = tid; i < n_frag; i += kThreads) {
             const uint32_t pix = s_frag[i].y & 0xFFFFFu, tri = s_frag[i].y >> 20;
             if (resolve_winner(s_wkey[pix]) == (int)tri) emit(pix, s_rec[tri].rgb);
           }
           if (r1 < n_live) {
             __syncthreads();
+#pragma unroll 1
             for (int i = tid; i < n_frag; i += kThreads) s_wkey[s_frag[i].y & 0xFFFFFu] = 0u;
           }
         } else {
