@@ -366,6 +366,7 @@ __device__ __forceinline__ void pixel_range(float mn, float mx, int lim, int &lo
 __device__ __forceinline__ void prepare_env(const RenderParams &p, int64_t env, int local_env,
                                          float4 *link_buf, DistSlot *s_dist, EnvShared &es,
                                          int lane, int64_t stride, bool write) {
+#pragma unroll 1
   for (int l = lane; l < p.nl; l += 32) {
     const double *pp = p.poses + (env * p.nl + l) * 3;
     const float th = (float)pp[2];  // poses.astype(float32), render.py:613
@@ -729,6 +730,7 @@ render_step_kernel(const RenderParams p) {
       // separable floor rays: t = -ez / dz and floor(wy) depend on the row
       // only (render.py:321-334), computed once per row by the last threads
       // (those with no or one vertex below)
+#pragma unroll 1
       for (int y = kThreads - 1 - tid; y < p.H; y += kThreads) {
         const double dy = s_floor[p.W + y], dz = s_floor[p.W + p.H + y];
         double t = 0.0;
@@ -744,14 +746,7 @@ render_step_kernel(const RenderParams p) {
         s_fk[y] = k;
       }
     }
-    for (int v = tid; v < p.nv; v += kThreads) {
-      float3 w;
-      if (v == tid) {  // the thread's first vertex: geometry held in registers
-        const float4 lk = s_lk[g_link];
-        w = make_float3(lk.x + g_bx * lk.z - g_bz * lk.w, g_by, lk.y + g_bx * lk.w + g_bz * lk.z);
-      } else {
-        w = world_vertex(p, s_lk, v);
-      }
+    auto project = [&](int v, const float3 w) {
       s_world[3 * v + 0] = w.x;
       s_world[3 * v + 1] = w.y;
       s_world[3 * v + 2] = w.z;
@@ -769,7 +764,16 @@ render_step_kernel(const RenderParams p) {
       s_vxy32[v] = make_float2(sx, sy);
       s_vxy64[v] = make_double2((double)sx, (double)sy);
       s_viz[v] = __drcp_rn((double)zv);  // iz = 1.0 / z (render.py:434-436)
+    };
+    if (tid < p.nv) {  // the thread's first vertex: geometry held in registers
+      const float4 lk = s_lk[g_link];
+      project(tid, make_float3(lk.x + g_bx * lk.z - g_bz * lk.w, g_by,
+                               lk.y + g_bx * lk.w + g_bz * lk.z));
     }
+    // (meshes of more than kThreads vertices; no strength-reduced induction
+    // variables for the common single pass above)
+#pragma unroll 1
+    for (int v = tid + kThreads; v < p.nv; v += kThreads) project(v, world_vertex(p, s_lk, v));
   };
 
   uint32_t vphase = 0;
