@@ -859,6 +859,7 @@ render_step_kernel(const RenderParams p) {
       // count and bbox-row total feed the block scan directly
       int my_live = 0, my_rows = 0;
       if (kBands && y0 > ystart && t0 < t1) load_tri(t0, n0, n1, n2);  // (first band: at the env's start)
+#pragma unroll 1
       for (int t = t0; t < t1; t++) {
         uint32_t rows = 0;
         const int i0 = n0, i1 = n1, i2 = n2;
@@ -1047,7 +1048,8 @@ render_step_kernel(const RenderParams p) {
           li = __shfl_sync(kFull, vi - v, warp) + wl - my_live;
           racc = (uint32_t)(__shfl_sync(kFull, ui - u, warp) + wr - my_rows);
         }
-        for (int t = t0; t < t1; t++) {
+#pragma unroll 1
+        for (int t = t0; t < t1; t++) {  // (per-thread block: ceil(nt / kThreads) triangles)
           const int r = s_rows[t];
           if (r != 0) {
             PXR_DCHECK(li < p.nt);
