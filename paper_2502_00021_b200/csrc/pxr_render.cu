@@ -525,7 +525,11 @@ __device__ __forceinline__ void put_rgb(uint8_t *col, uint32_t pix, uint32_t rgb
   col[3 * pix + 2] = (uint8_t)(rgb >> 16);
 }
 
-// Phase timer (debug): thread 0 adds the cycles since its last mark to a slot.
+// Phase timer (debug, libpxr_prof.so only: -DPXR_PHASE_PROF): thread 0 adds
+// the cycles since its last mark to a slot. Compiled out of libpxr.so (its
+// per-barrier pointer test cost ~7 instructions per warp and phase).
+#ifdef PXR_PHASE_PROF
+constexpr bool kPhaseProf = true;
 #define PXR_PROF(slot)                                  \
   do {                                                  \
     if (p.prof != nullptr && tid == 0) {                \
@@ -534,6 +538,12 @@ __device__ __forceinline__ void put_rgb(uint8_t *col, uint32_t pix, uint32_t rgb
       es.prof_t = now_;                                 \
     }                                                   \
   } while (0)
+#else
+constexpr bool kPhaseProf = false;
+#define PXR_PROF(slot) \
+  do {                 \
+  } while (0)
+#endif
 
 // kBands = false: the whole frame is one band (y0 = 0, straight-line code).
 // kFloor = draw_floor: the checker floor needs every thread for the
@@ -642,7 +652,7 @@ render_step_kernel(const RenderParams p) {
     fence_mbar_init();
     es.plan_ok = 0;
     for (int i = 0; i < kProfSlots; i++) es.prof[i] = 0;
-    es.prof_t = p.prof != nullptr ? clock64() : 0;
+    es.prof_t = kPhaseProf && p.prof != nullptr ? clock64() : 0;
   }
   __syncthreads();
   // Byte-permute plan of the NN video gather (distractor.py:172-176): with
@@ -1465,7 +1475,7 @@ render_step_kernel(const RenderParams p) {
   // the last frame store must have read shared memory before the CTA exits
   // (its global writes complete with the grid)
   if (tid == 0 && p.use_bulk) bulk_wait_read();
-  if (p.prof != nullptr) {
+  if (kPhaseProf && p.prof != nullptr) {
     PXR_PROF(7);  // the last store's shared-memory read
     if (tid == 0) es.prof[8] = local_env;
     __syncthreads();

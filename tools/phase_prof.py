@@ -1,10 +1,16 @@
 """Per-phase cycles of the fused render kernel (debug hook
 PXR_DEBUG_PROF: thread 0's clock at each phase-ending barrier, per CTA),
 averaged per env, plus the launch's device time with the host out of the
-loop (20 launches captured in one CUDA graph and replayed)."""
+loop (20 launches captured in one CUDA graph and replayed). Loads
+libpxr_prof.so (the timers are compiled out of libpxr.so) unless
+PXR_LIB_PATH names another build."""
 import argparse
 import os
 import sys
+
+os.environ.setdefault("PXR_LIB_PATH", os.path.join(
+    os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2502_00021_b200",
+    "libpxr_prof.so"))
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
