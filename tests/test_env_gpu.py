@@ -206,6 +206,42 @@ class TestStep:
         assert torch.equal(ov[fg], on[fg])
 
 
+@pytest.mark.parametrize("name,mode,batch", [("walker_lite", "video", 24), ("cheetah_lite", "none", 3),
+                                              ("hopper_lite", "color", 200)])
+def test_step_loop_same_without_programmatic_launch(E, knobs, name, mode, batch, tmp_path):
+    """The render launch with programmatic dependent launch (the default:
+    it may be scheduled while the physics / FK kernels before it run, and
+    waits for them before reading) against plain launches: the same obs,
+    rewards and state over a stretch of steps with resets."""
+    import torch
+
+    from paper_2502_00021_b200.bench_support import synthetic_pack
+    from paper_2502_00021_b200.video_pack import save_video_pack
+
+    kw = {}
+    if mode == "video":
+        path = tmp_path / "p.pxvp"
+        save_video_pack(synthetic_pack(), path)
+        kw["video_pack_path"] = str(path)
+    runs = []
+    for no_pdl in (None, 1):
+        knobs.set("PXR_DEBUG_NO_PDL", no_pdl)
+        env, s, obs = _env(E, name, batch=batch, seed=5, distractor_mode=mode, **kw)
+        gen = torch.Generator(device="cuda").manual_seed(1)
+        frames = [obs.clone()]
+        for _ in range(40):
+            act = torch.rand((batch, env.n_joints), generator=gen, device="cuda",
+                             dtype=torch.float64) * 2 - 1
+            s, out = E.step(env, s, act)
+            frames.append(out.obs.clone())
+        torch.cuda.synchronize()
+        runs.append((frames, s.sys.qpos.clone(), s.sys.qvel.clone()))
+    (fa, qa, va), (fb, qb, vb) = runs
+    for a, b in zip(fa, fb):
+        assert torch.equal(a, b)
+    assert torch.equal(qa, qb) and torch.equal(va, vb)
+
+
 class TestStepGraph:
     """StepGraph (policy -> step captured as one CUDA graph, replayed with the
     step key computed on the device) against the pure ``step`` loop."""
