@@ -434,39 +434,49 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 __device__ __forceinline__ void span_setup(const float2 a, const float2 b, const float2 c,
                                            float ymax, SpanRec &S) {
   const float2 v[3] = {a, b, c};
-  float ur0 = 0.0f, uc0 = 0.0f, ur1 = 0.0f, uc1 = 0.0f;
-  float lr0 = 0.0f, lc0 = 0.0f, lr1 = 0.0f, lc1 = 0.0f;
+  const float inf = __int_as_float(0x7f800000);
+  // unused slots bound nothing (x <= +inf, x >= -inf)
+  float ur0 = 0.0f, uc0 = inf, ur1 = 0.0f, uc1 = inf;
+  float lr0 = 0.0f, lc0 = -inf, lr1 = 0.0f, lc1 = -inf;
   bool have_u = false, have_l = false;
-  float ylo = -__int_as_float(0x7f800000), yhi = __int_as_float(0x7f800000);
+  float ylo = -inf, yhi = inf;
+  // branch-free: every edge's line is computed and the selects keep the
+  // ones its kind uses (the lanes of a warp hold triangles of every shape)
 #pragma unroll
   for (int k = 0; k < 3; k++) {
     const float2 s = v[k], t = v[(k + 1) % 3];
     const float A = t.x - s.x, B = t.y - s.y;
-    if (B == 0.0f) {
-      // horizontal edge: only the sign of A * (y - s.y) matters, and the f32
-      // comparison of y with s.y is exact
-      if (A > 0.0f) ylo = s.y; else yhi = s.y;
-    } else {
-      // an x bound whose slope only feeds a conservative bound: __fdividef's
-      // <= 2 ulp error moves the line by <= 2^-22 |r| (H + |s.y|), far
-      // inside m; folding m into the intercept adds one rounding of
-      // |c0 + m|, also far inside m
-      const float r = __fdividef(A, B);
-      const float c0 = __fmaf_rn(-r, s.y, s.x);
-      const float m = 0x1p-10f + (fabsf(s.x) + fabsf(r) * (fabsf(s.y) + ymax)) * 0x1p-17f;
-      if (B > 0.0f) {  // bounds x from above
-        ur1 = r; uc1 = c0 + m;
-        if (!have_u) { ur0 = r; uc0 = c0 + m; }
-        have_u = true;
-      } else {
-        lr1 = r; lc1 = c0 - m;
-        if (!have_l) { lr0 = r; lc0 = c0 - m; }
-        have_l = true;
-      }
-    }
+    // horizontal edge (B == 0): only the sign of A * (y - s.y) matters, and
+    // the f32 comparison of y with s.y is exact
+    const bool hz = B == 0.0f;
+    ylo = hz && A > 0.0f ? s.y : ylo;
+    yhi = hz && !(A > 0.0f) ? s.y : yhi;
+    // an x bound whose slope only feeds a conservative bound: the <= 1 ulp
+    // error of rcp.approx moves the line by <= 2^-22 |r| (H + |s.y|), far
+    // inside m; folding m into the intercept adds one rounding of |c0 + m|,
+    // also far inside m. A nearly horizontal edge (|r| >= 2^100, or r not
+    // finite: B == 0 or subnormal) bounds nothing -- dropping a bound only
+    // widens the span, and the exact test decides every span pixel.
+    float rb;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(B));
+    const float r = A * rb;
+    const bool ok = fabsf(r) < 0x1p100f;
+    const bool up = B > 0.0f && ok, dn = B < 0.0f && ok;
+    const float c0 = __fmaf_rn(-r, s.y, s.x);
+    const float m = __fmaf_rn(__fmaf_rn(fabsf(r), fabsf(s.y) + ymax, fabsf(s.x)), 0x1p-17f, 0x1p-10f);
+    const float cu = c0 + m, cl = c0 - m;
+    ur0 = up && !have_u ? r : ur0;  // the first edge of a kind fills both slots,
+    uc0 = up && !have_u ? cu : uc0;  // a second one the other
+    ur1 = up ? r : ur1;
+    uc1 = up ? cu : uc1;
+    have_u = have_u || up;
+    lr0 = dn && !have_l ? r : lr0;
+    lc0 = dn && !have_l ? cl : lc0;
+    lr1 = dn ? r : lr1;
+    lc1 = dn ? cl : lc1;
+    have_l = have_l || dn;
   }
-  // (a non-degenerate triangle has at least one edge of each kind; a single
-  // one is used twice)
+  // (a single edge of a kind is used twice)
   S.ur[0] = ur0; S.uc[0] = uc0; S.ur[1] = ur1; S.uc[1] = uc1;
   S.lr[0] = lr0; S.lc[0] = lc0; S.lr[1] = lr1; S.lc[1] = lc1;
   S.ylo = ylo;
