@@ -963,12 +963,24 @@ render_step_kernel(const RenderParams p) {
           // key store per group
           const float inf = __int_as_float(0x7f800000);
           const int n4 = npx >> 2;
+          // a background pixel is sky or one of the two checker greys: their
+          // final colours (colour distractor, then grayscale: as in emit) are
+          // computed once, each pixel selects one
+          auto final_of = [&](uint32_t c) {
+            if (p.mode == PXR_MODE_COLOR) c = __vsubus4(__vaddus4(c, bpos), bneg);
+            if (p.gray)  // env.py:168-173
+              c = (299u * (c & 0xffu) + 587u * ((c >> 8) & 0xffu) + 114u * ((c >> 16) & 0xffu) +
+                   500u) / 1000u;
+            return c;
+          };
+          const uint32_t f_sky = final_of(kSkyRGB), f_odd = final_of(122u * 0x010101u),
+                         f_even = final_of(158u * 0x010101u);
           for (int gi = first; gi < n4; gi += stride) {
             const int i0 = gi << 2;
             const int yb = (int)__umulhi((uint32_t)i0, p.wmagic), x = i0 - yb * p.W;
             const int k = s_fk[y0 + yb];
             float4 d4 = make_float4(inf, inf, inf, inf);
-            uint32_t c[4] = {kSkyRGB, kSkyRGB, kSkyRGB, kSkyRGB};
+            uint32_t c[4] = {f_sky, f_sky, f_sky, f_sky};
             if (k >= 0) {
               const double t = s_ft[y0 + yb];
               const float tf = (float)t;
@@ -979,20 +991,11 @@ render_step_kernel(const RenderParams p) {
 #pragma unroll
               for (int j = 0; j < 4; j++) {
                 const double wx = (double)ex + t * fx[j];
-                c[j] = (((uint32_t)__double2ll_rd(wx) ^ (uint32_t)k) & 1u ? 122u : 158u) * 0x010101u;
+                c[j] = ((uint32_t)__double2ll_rd(wx) ^ (uint32_t)k) & 1u ? f_odd : f_even;
               }
             }
-            if (p.mode == PXR_MODE_COLOR) {
-#pragma unroll
-              for (int j = 0; j < 4; j++) c[j] = __vsubus4(__vaddus4(c[j], bpos), bneg);
-            }
-            if (p.gray) {  // env.py:168-173, as in emit
-              uint32_t g4 = 0u;
-#pragma unroll
-              for (int j = 0; j < 4; j++)
-                g4 |= ((299u * (c[j] & 0xffu) + 587u * ((c[j] >> 8) & 0xffu) +
-                        114u * ((c[j] >> 16) & 0xffu) + 500u) / 1000u) << (8 * j);
-              reinterpret_cast<uint32_t *>(s_gray)[gi] = g4;
+            if (p.gray) {
+              reinterpret_cast<uint32_t *>(s_gray)[gi] = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
             } else {
               uint32_t *c3 = reinterpret_cast<uint32_t *>(s_col) + 3 * gi;
               c3[0] = c[0] | (c[1] << 24);
