@@ -123,9 +123,9 @@ struct __align__(16) SpanRec {
   uint32_t row0;       // first row unit of the triangle in the round
 };
 static_assert(sizeof(SpanRec) == 48, "SpanRec layout");
-// Non-empty spans wait in a per-warp queue as uint2 {x0 | len << 16,
-// row | live_tri << 16} until 32 can be evaluated together.
-constexpr int kQueue = 64;
+// Raster candidates wait in a CTA-wide pool as pix | live_tri << 20 (the
+// same footprint as the per-warp span queues it replaced).
+constexpr int kPoolCap = 3072;
 
 // A covered fragment: uint2 {RN32(z) bits | (z < RN32(z)) << 31, pix | tri << 20}
 // (depths are positive, so the f32 sign bit is free; pix < 2^20 and the
@@ -219,7 +219,7 @@ __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   L.rec = o;    o += p.cap * (int)sizeof(TriRec);
   L.span = o;   o += align_up(p.cap * (int)sizeof(SpanRec), 16);
   L.rowner = o; o += align_up((p.row_cap / 32 + 2) * 2, 16);
-  L.queue = o;  o += kWarps * kQueue * 8;
+  L.queue = o;  o += kPoolCap * 4;  // the raster's candidate pool
   L.frag = o;   o += kFragCap * 8;
   L.depth = o;  o += align_up(npx * 4, 16);
   L.col = o;    o += align_up(npx * 3, 16);
@@ -246,11 +246,13 @@ struct EnvShared {
   int n_live;
   int round_end;
   int n_frag;
+  int n_pool;  // raster candidates appended to s_pool (may exceed kPoolCap: the rest ran in place)
   int one_round;  // all live triangles of the band fit one raster round
   int plan_ok;
   int st[kStats];  // debug counters (p.stats)
   long long prof[kProfSlots];  // debug phase cycles (p.prof)
   long long prof_t;
+  long long rmin, rmax;  // debug (libpxr_prof.so): raster phase A / B ends (last worker)
 };
 
 // Per-env distractor step (writes the new state back to HBM):
@@ -600,7 +602,7 @@ render_step_kernel(const RenderParams p) {
   TriRec *s_rec = reinterpret_cast<TriRec *>(smem + L.rec);
   SpanRec *s_span = reinterpret_cast<SpanRec *>(smem + L.span);
   uint16_t *s_rowner = reinterpret_cast<uint16_t *>(smem + L.rowner);
-  uint2 *s_queue = reinterpret_cast<uint2 *>(smem + L.queue);
+  uint32_t *s_pool = reinterpret_cast<uint32_t *>(smem + L.queue);  // pix | live tri << 20
   uint2 *s_frag = reinterpret_cast<uint2 *>(smem + L.frag);
   float *s_depth = reinterpret_cast<float *>(smem + L.depth);
   uint32_t *s_dbits = reinterpret_cast<uint32_t *>(smem + L.depth);
@@ -662,6 +664,8 @@ render_step_kernel(const RenderParams p) {
     fence_mbar_init();
     es.plan_ok = 0;
     for (int i = 0; i < kProfSlots; i++) es.prof[i] = 0;
+    es.rmin = 0;
+    es.rmax = 0;
     es.prof_t = kPhaseProf && p.prof != nullptr ? clock64() : 0;
   }
   __syncthreads();
@@ -1091,6 +1095,7 @@ render_step_kernel(const RenderParams p) {
           if (fast) {
             es.round_end = li;
             es.n_frag = 0;
+            es.n_pool = 0;
           }
         }
       }
@@ -1122,6 +1127,7 @@ render_step_kernel(const RenderParams p) {
             }
             es.round_end = lo;
             es.n_frag = 0;
+            es.n_pool = 0;
           }
           __syncthreads();
         }
@@ -1228,11 +1234,14 @@ render_step_kernel(const RenderParams p) {
         PXR_PROF(3);  // records + span equations (+ video / sky background)
 
         // (triangle, bbox row) units, 32 per chunk, chunks dealt round-robin
-        // to the warps: each lane computes one row's conservative span and the
-        // non-empty spans go to the warp's queue; whenever 32 are queued (and
-        // at the end) the warp expands 32 spans into pixel candidates and runs
-        // the exact test on them, so the f64 work runs on full warps even
-        // though most rows of the thin triangles hold no pixel centre.
+        // to the warps: each lane computes one row's conservative span, and
+        // the chunk's non-empty spans become (pixel, live triangle)
+        // candidates in a CTA-wide pool (single-pixel spans directly, longer
+        // ones through a warp scan + owner search); after a barrier every
+        // thread runs the exact test on pooled candidates. Most rows of the
+        // thin triangles hold no pixel centre, so the f64 work only sees real
+        // candidates, and it is balanced over the CTA whatever the triangle
+        // sizes (a large triangle's rows no longer keep one warp busy).
         const int n_chunks = (n_rows + 31) >> 5;
         // while warp kWarps-1 prepares the next env the chunks are dealt to
         // the other warps only (it would otherwise finish last)
@@ -1240,11 +1249,21 @@ render_step_kernel(const RenderParams p) {
         // must be CTA-uniform, also in a second raster round)
         const bool preparing = !prepared;
         const int n_workers = preparing ? kWarps - 1 : kWarps;
-        if (warp == kWarps - 1 && preparing)
+#ifdef PXR_PHASE_PROF
+        const long long r_t0 = clock64();
+#endif
+        if (warp == kWarps - 1 && preparing) {
           prepare_env(p, env + env_stride, local_env + 1, s_link + (cb ^ 1) * p.nl, s_dist, es,
                       lane, env_stride, dist_write);
+#ifdef PXR_PHASE_PROF
+          if (p.prof != nullptr && lane == 0)  // slot 9: the next env's preparation
+            atomicAdd(reinterpret_cast<unsigned long long *>(&es.prof[9]),
+                      (unsigned long long)(clock64() - r_t0));
+#endif
+        }
+        const bool prof_worker = !(warp == kWarps - 1 && preparing);
+        (void)prof_worker;
         prepared = true;
-        uint2 *q = s_queue + warp * 64;
         // a covered candidate: min-reduce its f32 depth into the pixel and
         // take a fragment-list slot (ptxas aggregates the warp's increments
         // into one shared atomic)
@@ -1257,13 +1276,12 @@ render_step_kernel(const RenderParams p) {
             s_frag[slot] = make_uint2(zb | (z < (double)zf ? 0x80000000u : 0u),
                                       pix | ((uint32_t)tri << 20));
         };
-        int qn = 0;  // queued spans (warp-uniform)
-        bool more = true;
-        int k = warp - n_workers;
-        while (more) {
-          k += n_workers;  // static round-robin over the chunks
-          more = k < n_chunks && warp < n_workers;
-          if (more) {
+        if (warp < n_workers) {
+          // Phase A: each chunk's 32 row spans are expanded (warp scan of
+          // their lengths + owner search) into (pixel, live triangle)
+          // candidates appended to the CTA-wide pool -- a large triangle's
+          // pixels no longer stay with the warp that drew its rows.
+          for (int k = warp; k < n_chunks; k += n_workers) {  // static round-robin
             const int u = k * 32 + lane;
             // owner triangle of unit u: the owner of the chunk's first unit plus
             // the triangles starting inside the chunk up to u (all have >= 1 row)
@@ -1287,54 +1305,34 @@ render_step_kernel(const RenderParams p) {
               PXR_DCHECK(row >= y0 && row < y1);
               PXR_DCHECK(len == 0 || (x0 >= 0 && x0 + len <= p.W && len < 0x10000));
             }
-            const uint32_t sm = __ballot_sync(kFull, len > 0);
-            if (len > 0)
-              q[qn + __popc(sm & lanemask_lt)] =
-                  make_uint2((uint32_t)x0 | ((uint32_t)len << 16), (uint32_t)row | ((uint32_t)j << 16));
-            qn += __popc(sm);
-            if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[2], __popc(sm));
-            PXR_DCHECK(qn <= kQueue);
-          }
-          while (qn >= 32 || (!more && qn > 0)) {
-            __syncwarp();
-            const int nb = min(qn, 32);
-            qn -= nb;
-            int len = 0, x0 = 0, row = 0, j = 0;
-            if (lane < nb) {
-              const uint2 sp = q[qn + lane];
-              x0 = (int)(sp.x & 0xffffu);
-              len = (int)(sp.x >> 16);
-              row = (int)(sp.y & 0xffffu);
-              j = (int)(sp.y >> 16);
-            }
-            __syncwarp();
-            if (more) {
-              // steady state (32 spans queued): each lane tests the first
-              // pixel of its own span -- a full round of 32 candidates with
-              // no expansion scan or owner search -- and re-queues the span's
-              // remaining pixels (most spans hold one pixel)
-              PXR_DCHECK(nb == 32 && len > 0);
-              if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[3], 32);
-              const uint32_t pix = (uint32_t)((row - y0) * p.W + x0);
-              PXR_DCHECK(pix < (uint32_t)npx && j < n_round);
-              double z;
-              if (eval_exact(s_rec[j], x0, row, s_vxy64, s_viz, z)) add_fragment(z, pix, j);
-              const bool keep = len > 1;
-              const uint32_t km = __ballot_sync(kFull, keep);
-              if (keep)
-                q[qn + __popc(km & lanemask_lt)] =
-                    make_uint2((uint32_t)(x0 + 1) | ((uint32_t)(len - 1) << 16),
-                               (uint32_t)row | ((uint32_t)j << 16));
-              qn += __popc(km);
-              PXR_DCHECK(qn <= kQueue);
+            if (kWithStats && p.stats != nullptr && lane == 0)
+              atomicAdd(&es.st[2], __popc(__ballot_sync(kFull, len > 0)));
+            if (__all_sync(kFull, len <= 1)) {
+              // every span is one pixel or empty (the common case): the
+              // spans are the candidates, no expansion
+              const uint32_t sm = __ballot_sync(kFull, len > 0);
+              const int n = __popc(sm);
+              if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[3], n);
+              int base = 0;
+              if (lane == 0 && n > 0) base = atomicAdd(&es.n_pool, n);
+              base = __shfl_sync(kFull, base, 0) + __popc(sm & lanemask_lt);
+              if (len > 0) {
+                const uint32_t pix = (uint32_t)((row - y0) * p.W + x0);
+                PXR_DCHECK(pix < (uint32_t)npx && j < n_round);
+                if (base < kPoolCap) {
+                  s_pool[base] = pix | ((uint32_t)j << 20);
+                } else {  // pool full: evaluated here
+                  double z;
+                  if (eval_exact(s_rec[j], x0, row, s_vxy64, s_viz, z)) add_fragment(z, pix, j);
+                }
+              }
               continue;
             }
-            // draining the queue: expand the spans into pixel candidates
             const int incl = warp_incl_scan(len, lane);
             const int excl = incl - len;
-            const int N = __shfl_sync(kFull, incl, 31);
-            const int NE = N;
+            const int NE = __shfl_sync(kFull, incl, 31);
             if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[3], NE);
+#pragma unroll 1
             for (int c0 = 0; c0 < NE; c0 += 32) {
               // span lane of candidate c = c0 + lane: the number of lanes whose
               // inclusive end is <= c (branch-free binary search over the scan)
@@ -1349,20 +1347,58 @@ render_step_kernel(const RenderParams p) {
               const int o_x0 = __shfl_sync(kFull, x0, owner & 31);
               const int o_row = __shfl_sync(kFull, row, owner & 31);
               const int o_tri = __shfl_sync(kFull, j, owner & 31);
-              bool cov = false;
-              uint32_t pix = 0;
-              double z = 0.0;
+              int base = 0;
+              if (lane == 0) base = atomicAdd(&es.n_pool, min(32, NE - c0));
+              base = __shfl_sync(kFull, base, 0);
               if (c < NE) {
                 const int px = o_x0 + (c - o_ex);
-                pix = (uint32_t)((o_row - y0) * p.W + px);
+                const uint32_t pix = (uint32_t)((o_row - y0) * p.W + px);
                 PXR_DCHECK(pix < (uint32_t)npx && o_tri < n_round && owner < 32);
-                cov = eval_exact(s_rec[o_tri], px, o_row, s_vxy64, s_viz, z);
+                if (base + lane < kPoolCap) {
+                  s_pool[base + lane] = pix | ((uint32_t)o_tri << 20);
+                } else {  // pool full: evaluated here
+                  double z;
+                  if (eval_exact(s_rec[o_tri], px, o_row, s_vxy64, s_viz, z))
+                    add_fragment(z, pix, o_tri);
+                }
               }
-              if (cov) add_fragment(z, pix, o_tri);
             }
           }
+#ifdef PXR_PHASE_PROF
+          if (p.prof != nullptr && lane == 0) atomicMax(&es.rmin, clock64() - r_t0);  // phase A end
+#endif
         }
+        {
+          // Phase B, every warp (the one that prepared the next env too): the
+          // reference's exact f64 edge / barycentric / depth test on the
+          // pooled candidates, one per thread
+          __syncthreads();
+          const int n_pool = min(es.n_pool, kPoolCap);
+#pragma unroll 1
+          for (int i = tid; i < n_pool; i += kThreads) {
+            const uint32_t w = s_pool[i];
+            const uint32_t pix = w & 0xFFFFFu;
+            const int tri = (int)(w >> 20);
+            const int yb = (int)__umulhi(pix, p.wmagic);
+            const int px = (int)pix - yb * p.W;
+            PXR_DCHECK(pix < (uint32_t)npx && tri < n_round);
+            double z;
+            if (eval_exact(s_rec[tri], px, y0 + yb, s_vxy64, s_viz, z)) add_fragment(z, pix, tri);
+          }
+        }
+#ifdef PXR_PHASE_PROF
+        if (p.prof != nullptr && lane == 0)  // slots 10 / 11: phase A / B ends
+          atomicMax(&es.rmax, clock64() - r_t0);
+#endif
         __syncthreads();
+#ifdef PXR_PHASE_PROF
+        if (p.prof != nullptr && tid == 0) {
+          es.prof[10] += es.rmin;
+          es.prof[11] += es.rmax;
+          es.rmin = 0;
+          es.rmax = 0;
+        }
+#endif
         PXR_PROF(4);  // row spans -> candidates -> exact test -> fragments
         // the upscaled video frame must have landed before the paint
         if (!kBands && p.hw && r0 == 0) mbar_wait_parity(&es.vbar, vpar);

@@ -66,3 +66,7 @@ for case in a.cases:
     for i, n in enumerate(SLOTS):
         c = P[:, i].mean()
         print(f"   {n:24s} {c / 1965:8.2f} us/CTA  {c / (envs / len(P)):8.0f} cyc/env  {100 * c / tot:5.1f} %")
+    per = envs / len(P)
+    print(f"   raster detail per env: rows drawn {P[:, 10].mean() / per:6.0f} cyc, pool "
+          f"evaluated {P[:, 11].mean() / per:6.0f} cyc, next-env preparation (1 warp) "
+          f"{P[:, 9].mean() / per:6.0f} cyc")
