@@ -60,7 +60,19 @@ def main():
             iters = max(5, min(200, 200000 // b))
             w.precompute_keys(range(3, 3 + iters))  # host Threefry out of the timed loop
             ms_r = time_events(lambda i: w.render(poses[i % 2], 3 + i), iters)
-            del w, poses
+            # the same launches captured in a CUDA graph (20 per replay): the
+            # device time without the Python launch loop
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(st):
+                with torch.cuda.graph(gr, stream=st):
+                    for i in range(20):
+                        w.render(poses[i % 2], 3 + i, stream=st)
+            torch.cuda.current_stream().wait_stream(st)
+            gr.replay()
+            ms_rg = time_events(lambda i: gr.replay(), max(3, iters // 20)) / 20
+            del gr, w, poses
             # full env step + conv-stub policy (device-resident loop)
             cfg = E.EnvConfig(model=STANDIN_MODELS.get(env_model, env_model), batch=b,
                               distractor_mode=mode,
@@ -85,9 +97,9 @@ def main():
             iters_g = max(20, min(1000, 200000 // b))
             ms_g = time_events(lambda i: g.replay(1), iters_g)
             rows.append((name, mode, b, b / ms_r * 1e3, ms_r, b / ms_s * 1e3, ms_s,
-                         b / ms_g * 1e3, ms_g))
+                         b / ms_g * 1e3, ms_g, b / ms_rg * 1e3, ms_rg))
             print(f"{name:12s} {mode:6s} B={b:6d}  render {b / ms_r * 1e3:12.0f} env-steps/s "
-                  f"({ms_r:.3f} ms)  env_step+policy {b / ms_s * 1e3:12.0f} ({ms_s:.3f} ms)  "
+                  f"({ms_r:.3f} ms; graphed {b / ms_rg * 1e3:.0f}, {ms_rg * 1e3:.1f} us)  env_step+policy {b / ms_s * 1e3:12.0f} ({ms_s:.3f} ms)  "
                   f"graphed {b / ms_g * 1e3:12.0f} ({ms_g:.3f} ms)", flush=True)
             del g
             del env, state, obs, box
@@ -95,16 +107,18 @@ def main():
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out + ".csv", "w") as f:
         f.write("model,mode,envs,render_sps,render_ms,env_step_policy_sps,env_step_policy_ms,"
-                "graphed_sps,graphed_ms\n")
+                "graphed_sps,graphed_ms,render_graphed_sps,render_graphed_ms\n")
         for r in rows:
             f.write(f"{r[0]},{r[1]},{r[2]},{r[3]:.6g},{r[4]:.6g},{r[5]:.6g},{r[6]:.6g},"
-                    f"{r[7]:.6g},{r[8]:.6g}\n")
+                    f"{r[7]:.6g},{r[8]:.6g},{r[9]:.6g},{r[10]:.6g}\n")
     with open(a.out + ".md", "w") as f:
-        f.write("| model | distractors | envs | rendered env-steps/s | ms | env step + conv policy, "
+        f.write("| model | distractors | envs | rendered env-steps/s (host loop) | ms | rendered, "
+                "launches in a CUDA graph | ms | env step + conv policy, "
                 "env-steps/s | ms | same, one CUDA graph per step | ms |\n"
-                "|---|---|---|---|---|---|---|---|---|\n")
+                "|---|---|---|---|---|---|---|---|---|---|---|\n")
         for r in rows:
-            f.write(f"| {r[0]} | {r[1]} | {r[2]} | {r[3]:,.0f} | {r[4]:.3f} | {r[5]:,.0f} | "
+            f.write(f"| {r[0]} | {r[1]} | {r[2]} | {r[3]:,.0f} | {r[4]:.3f} | {r[9]:,.0f} | "
+                    f"{r[10]:.4f} | {r[5]:,.0f} | "
                     f"{r[6]:.3f} | {r[7]:,.0f} | {r[8]:.3f} |\n")
 
 
