@@ -32,13 +32,13 @@
 //      colour, the degenerate-normal cull) plus f32 line equations for
 //      conservative row spans; (triangle, bbox row) units in 32-row chunks
 //      dealt to the warps: each lane computes one row's conservative span,
-//      non-empty spans gather in a per-warp queue; whenever 32 are queued
-//      each lane tests the first pixel of one span (a full round of 32
-//      candidates with no expansion) and re-queues the span's remaining
-//      pixels; at the end the queue is drained with a warp scan + owner
-//      search expanding the spans into whole rounds of candidates; every
-//      candidate gets the reference's exact f64 edge / barycentric / depth
-//      arithmetic; covered fragments min-reduce their f32 depth per pixel
+//      and a chunk's non-empty spans become (pixel, triangle) candidates in
+//      a CTA-wide pool (single-pixel spans directly, longer ones through a
+//      warp scan + owner search); after a barrier every thread takes pooled
+//      candidates, so the f64 work is balanced over the CTA however the
+//      triangles' rows fall on the warps; every candidate gets the
+//      reference's exact f64 edge / barycentric / depth arithmetic;
+//      covered fragments min-reduce their f32 depth per pixel
 //      with a 32-bit shared-memory atomicMin and are appended to a fragment
 //      list;
 //   4. exact order-independent resolve of the reference's SEQUENTIAL strict
@@ -124,7 +124,8 @@ struct __align__(16) SpanRec {
 };
 static_assert(sizeof(SpanRec) == 48, "SpanRec layout");
 // Raster candidates wait in a CTA-wide pool as pix | live_tri << 20 (the
-// same footprint as the per-warp span queues it replaced).
+// footprint of the per-warp span queues it replaced; a full pool leaves the
+// rest to the warp that drew them).
 constexpr int kPoolCap = 3072;
 
 // A covered fragment: uint2 {RN32(z) bits | (z < RN32(z)) << 31, pix | tri << 20}
@@ -136,7 +137,7 @@ constexpr int kMinSplitRows = 12;
 
 // Shared-memory offsets of one CTA (smem_layout).
 struct SmemLayout {
-  int link, floor, maps, vxy64, viz, vxy32, vz, world, tris, rows, ids, lrp, rec, span, rowner, queue,
+  int link, floor, maps, vxy64, viz, vxy32, vz, world, tris, rows, ids, lrp, rec, span, rowner, pool,
       frag, depth, col, wkey, gray, gplan, vframe, total;
 };
 
@@ -219,7 +220,7 @@ __host__ __device__ inline SmemLayout smem_layout(const RenderParams &p) {
   L.rec = o;    o += p.cap * (int)sizeof(TriRec);
   L.span = o;   o += align_up(p.cap * (int)sizeof(SpanRec), 16);
   L.rowner = o; o += align_up((p.row_cap / 32 + 2) * 2, 16);
-  L.queue = o;  o += kPoolCap * 4;  // the raster's candidate pool
+  L.pool = o;   o += kPoolCap * 4;  // the raster's candidate pool
   L.frag = o;   o += kFragCap * 8;
   L.depth = o;  o += align_up(npx * 4, 16);
   L.col = o;    o += align_up(npx * 3, 16);
@@ -602,7 +603,7 @@ render_step_kernel(const RenderParams p) {
   TriRec *s_rec = reinterpret_cast<TriRec *>(smem + L.rec);
   SpanRec *s_span = reinterpret_cast<SpanRec *>(smem + L.span);
   uint16_t *s_rowner = reinterpret_cast<uint16_t *>(smem + L.rowner);
-  uint32_t *s_pool = reinterpret_cast<uint32_t *>(smem + L.queue);  // pix | live tri << 20
+  uint32_t *s_pool = reinterpret_cast<uint32_t *>(smem + L.pool);  // pix | live tri << 20
   uint2 *s_frag = reinterpret_cast<uint2 *>(smem + L.frag);
   float *s_depth = reinterpret_cast<float *>(smem + L.depth);
   uint32_t *s_dbits = reinterpret_cast<uint32_t *>(smem + L.depth);
