@@ -640,12 +640,16 @@ __global__ void fk_env_kernel(const double *qpos, const int32_t *parent, const d
   }
 }
 
-// Lanes per env by batch (tools/phys_bench.py on a B200, Humanoid / HalfCheetah):
-// one warp per env is fastest up to ~1k envs (B=1: 0.17 / 0.10 ms against
-// 0.65 / 0.25 ms for one thread per env), half a warp up to 2k, a quarter
-// warp up to ~6k for models of 10+ dofs (B=4096: 0.57 against 0.76 ms), one
-// thread per env above (B=16384: 1.05 against 1.76 ms for a quarter warp).
-constexpr int64_t kWarpEnvMax = 1024, kHalfEnvMax = 2048, kQuarterEnvMax = 6144;
+// Lanes per env by batch (tools/phys_bench.py on a B200, Humanoid / HalfCheetah,
+// round 2): half a warp per env with the smallest shared-memory carveout (the
+// lanes' RNEA state stays in L1) up to two waves of 8-env blocks (B=1: 0.16 /
+// 0.10 ms against 0.65 / 0.25 ms for one thread per env; B=1000: 0.17 /
+// 0.10; B=2048: 0.34 / 0.19), then a quarter warp up to ~6k for models of
+// 10+ dofs (B=4096: 0.58 against 0.79 ms), one thread per env above
+// (B=16384: 1.04 against 1.77 ms for a quarter warp). One warp per env
+// (same carveout) is as fast as half a warp up to ~600 envs and is kept for
+// PXR_DEBUG_PHYS=warp.
+constexpr int64_t kHalfEnvMax = 2368, kQuarterEnvMax = 6144;
 
 static inline unsigned blocks_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
@@ -691,22 +695,24 @@ extern "C" pxr_status pxr_physics_step(const pxr_model *model, double *qpos, dou
   // (throughput); PXR_DEBUG_PHYS=warp|half|quarter|thread forces one
   const char *force = debug_knob(kDbgPhys);
   const int nd = model->n_links + 2;
-  char kind = batch <= kWarpEnvMax                  ? 'w'
-              : batch <= kHalfEnvMax                  ? 'h'
+  char kind = batch <= kHalfEnvMax                    ? 'h'
               : (nd >= 12 && batch <= kQuarterEnvMax) ? 'q'
                                                       : 't';
   if (force != nullptr) kind = force[0];
   cudaStream_t st = (cudaStream_t)stream;
   {
-    // warp per env: the lanes' RNEA state lives in local memory (L1), so
-    // ask for the smallest shared-memory carveout (set once per device; at
-    // ~100 envs the default split left the 4 warps' working set spilling
-    // to L2: Humanoid B=100 0.32 -> 0.17 ms). The sub-warp kernels keep the
-    // default (their occupancy needs the shared memory).
+    // warp / half warp per env: the lanes' RNEA state lives in local memory
+    // (L1), so ask for the smallest shared-memory carveout (set once per
+    // device; at ~100 envs the default split left the warps' working set
+    // spilling to L2: Humanoid B=100 0.32 -> 0.17 ms). The quarter-warp
+    // kernel keeps the default (at its batches occupancy needs the shared
+    // memory: B=4096 0.58 against 0.75 ms).
     static bool carveout_set[64] = {};
     const DeviceFacts &df = device_facts();
     if (!carveout_set[df.device & 63]) {
       cudaFuncSetAttribute((const void *)physics_step_warp_kernel<32>,
+                           cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+      cudaFuncSetAttribute((const void *)physics_step_warp_kernel<16>,
                            cudaFuncAttributePreferredSharedMemoryCarveout, 0);
       (void)cudaGetLastError();
       carveout_set[df.device & 63] = true;

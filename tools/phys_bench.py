@@ -8,7 +8,7 @@ from paper_2502_00021_b200 import _native
 from paper_2502_00021_b200.models import STANDIN_MODELS
 L = _native.lib()
 for model in ("humanoid_lite", "cheetah_lite"):
-    for B in (1, 10, 100, 1000, 4096, 16384, 65536):
+    for B in [int(x) for x in os.environ.get("PHYS_BATCHES", "1 10 100 1000 4096 16384 65536").split()]:
         env, s, obs = E.make_env(E.EnvConfig(model=STANDIN_MODELS.get(model, model), batch=B))
         act = torch.zeros((B, env.n_joints), dtype=torch.float64, device='cuda')
         res = []
