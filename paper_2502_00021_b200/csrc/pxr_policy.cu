@@ -272,12 +272,70 @@ conv_feat_tc_kernel(const uint8_t *__restrict__ obs, int64_t batch, int H, int W
 
 constexpr int kProjEnvs = 16;
 constexpr int kProjTile = 256;  // proj rows per shared-memory tile
+// The features of an env are reduced in slices of kProjSliceTiles tiles: lane
+// l chains the features k = l (mod 32) of the slice in ascending order (one
+// FMA chain per output), a fixed xor tree sums the lanes, and the slice sums
+// are added in slice order -- the same arithmetic whether one CTA walks all
+// slices of its envs (large batches) or each slice runs on its own CTA and
+// a combine kernel adds them (small batches), so a row never depends on the
+// batch it is in.
+constexpr int kProjSliceTiles = 8;
+constexpr int kProjSlice = kProjTile * kProjSliceTiles;
 
 // JP = J rounded up to a multiple of 4: the staged proj rows are padded with
 // zeros to JP floats so each lane reads its row with 128-bit loads (rows
 // 16 B-aligned; 8 consecutive rows of a quarter-warp hit distinct banks for
 // every JP used) and the FMA chain of each real output j < J is exactly the
 // unpadded one.
+//
+// Features [ks, ke) of the CTA's envs against proj: per-lane FMA chains,
+// reduced over the warp; lane j returns output j's sum.
+template <int JP>
+__device__ __forceinline__ float proj_slice(const float *__restrict__ fr, bool active, int ks,
+                                            int ke, const float *__restrict__ proj, int J,
+                                            float *s_p, int tid, int lane) {
+  float pacc[JP];
+#pragma unroll
+  for (int j = 0; j < JP; j++) pacc[j] = 0.0f;
+  for (int k0 = ks; k0 < ke; k0 += kProjTile) {
+    const int kn = min(kProjTile, ke - k0);
+    __syncthreads();  // previous tile no longer read
+    for (int i = tid; i < kn * JP; i += kProjEnvs * 32) {
+      const int r = i / JP, j = i - r * JP;
+      s_p[i] = j < J ? __ldg(proj + (int64_t)(k0 + r) * J + j) : 0.0f;
+    }
+    __syncthreads();
+    if (active) {
+      // (unrolled: several feature loads in flight; each output's FMA
+      // chain keeps its order)
+#pragma unroll 4
+      for (int kk = lane; kk < kn; kk += 32) {
+        const float v = __ldg(fr + k0 + kk);
+        const float4 *pr = reinterpret_cast<const float4 *>(s_p + kk * JP);
+#pragma unroll
+        for (int j4 = 0; j4 < JP / 4; j4++) {
+          const float4 w = pr[j4];
+          pacc[4 * j4 + 0] = __fmaf_rn(v, w.x, pacc[4 * j4 + 0]);
+          pacc[4 * j4 + 1] = __fmaf_rn(v, w.y, pacc[4 * j4 + 1]);
+          pacc[4 * j4 + 2] = __fmaf_rn(v, w.z, pacc[4 * j4 + 2]);
+          pacc[4 * j4 + 3] = __fmaf_rn(v, w.w, pacc[4 * j4 + 3]);
+        }
+      }
+    }
+  }
+  float mine = 0.0f;
+#pragma unroll
+  for (int j = 0; j < JP; j++) {
+    float v = pacc[j];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == j) mine = v;
+  }
+  return mine;
+}
+
+// Projection + tanh, one warp per env (kProjEnvs per CTA, sharing the staged
+// proj tiles): all slices in order.
 template <int JP>
 __global__ void __launch_bounds__(kProjEnvs * 32)
 conv_proj_kernel(const float *__restrict__ feat, int64_t batch, int K,
@@ -290,46 +348,42 @@ conv_proj_kernel(const float *__restrict__ feat, int64_t batch, int K,
        e0 += (int64_t)gridDim.x * kProjEnvs) {
     const int64_t env = e0 + warp;
     const float *fr = feat + env * (int64_t)K;
-    float pacc[JP];
-#pragma unroll
-    for (int j = 0; j < JP; j++) pacc[j] = 0.0f;
-    for (int k0 = 0; k0 < K; k0 += kProjTile) {
-      const int kn = min(kProjTile, K - k0);
-      __syncthreads();  // previous tile no longer read
-      for (int i = tid; i < kn * JP; i += kProjEnvs * 32) {
-        const int r = i / JP, j = i - r * JP;
-        s_p[i] = j < J ? __ldg(proj + (int64_t)(k0 + r) * J + j) : 0.0f;
-      }
-      __syncthreads();
-      if (env < batch) {
-        // (unrolled: several feature loads in flight; each output's FMA
-        // chain keeps its order)
-#pragma unroll 4
-        for (int kk = lane; kk < kn; kk += 32) {
-          const float v = __ldg(fr + k0 + kk);
-          const float4 *pr = reinterpret_cast<const float4 *>(s_p + kk * JP);
-#pragma unroll
-          for (int j4 = 0; j4 < JP / 4; j4++) {
-            const float4 w = pr[j4];
-            pacc[4 * j4 + 0] = __fmaf_rn(v, w.x, pacc[4 * j4 + 0]);
-            pacc[4 * j4 + 1] = __fmaf_rn(v, w.y, pacc[4 * j4 + 1]);
-            pacc[4 * j4 + 2] = __fmaf_rn(v, w.z, pacc[4 * j4 + 2]);
-            pacc[4 * j4 + 3] = __fmaf_rn(v, w.w, pacc[4 * j4 + 3]);
-          }
-        }
-      }
-    }
-    if (env < batch) {
-#pragma unroll
-      for (int j = 0; j < JP; j++) {
-        if (j >= J) break;
-        float v = pacc[j];
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == j) out[env * J + j] = (double)tanhf(v);
-      }
-    }
+    float total = 0.0f;  // lane j: output j
+    for (int ks = 0; ks < K; ks += kProjSlice)
+      total += proj_slice<JP>(fr, env < batch, ks, min(ks + kProjSlice, K), proj, J, s_p, tid, lane);
+    if (env < batch && lane < J) out[env * J + lane] = (double)tanhf(total);
   }
+}
+
+// Small batches: CTA (group, slice) reduces one slice of its kProjEnvs envs
+// and parks the sums in the env's own (already read) feature slots k = ks + j.
+template <int JP>
+__global__ void __launch_bounds__(kProjEnvs * 32)
+conv_proj_slice_kernel(float *__restrict__ feat, int64_t batch, int K,
+                       const float *__restrict__ proj, int J) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  float *s_p = reinterpret_cast<float *>(sm);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t env = (int64_t)blockIdx.x * kProjEnvs + warp;
+  const int ks = blockIdx.y * kProjSlice;
+  float *fr = feat + env * (int64_t)K;
+  const float sum = proj_slice<JP>(fr, env < batch, ks, min(ks + kProjSlice, K), proj, J, s_p,
+                                   tid, lane);
+  __syncwarp();  // every lane has read the slice's features
+  if (env < batch && lane < J) fr[ks + lane] = sum;
+}
+
+// ... and the slice sums are added in slice order (one thread per output).
+__global__ void conv_proj_combine_kernel(const float *__restrict__ feat, int64_t batch, int K,
+                                         int J, double *__restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= batch * J) return;
+  const int64_t env = i / J;
+  const int j = (int)(i - env * J);
+  const float *fr = feat + env * (int64_t)K;
+  float total = 0.0f;
+  for (int ks = 0; ks < K; ks += kProjSlice) total += fr[ks + j];
+  out[i] = (double)tanhf(total);
 }
 
 }  // namespace pxr
@@ -397,15 +451,16 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   const int jp = (n_joints + 3) & ~3;
   const int psmem = kProjTile * jp * (int)sizeof(float);
   void (*pk)(const float *, int64_t, int, const float *, int, double *) = nullptr;
+  void (*sk)(float *, int64_t, int, const float *, int) = nullptr;
   switch (jp) {
-    case 4: pk = conv_proj_kernel<4>; break;
-    case 8: pk = conv_proj_kernel<8>; break;
-    case 12: pk = conv_proj_kernel<12>; break;
-    case 16: pk = conv_proj_kernel<16>; break;
-    case 20: pk = conv_proj_kernel<20>; break;
-    case 24: pk = conv_proj_kernel<24>; break;
-    case 28: pk = conv_proj_kernel<28>; break;
-    default: pk = conv_proj_kernel<32>; break;
+    case 4: pk = conv_proj_kernel<4>; sk = conv_proj_slice_kernel<4>; break;
+    case 8: pk = conv_proj_kernel<8>; sk = conv_proj_slice_kernel<8>; break;
+    case 12: pk = conv_proj_kernel<12>; sk = conv_proj_slice_kernel<12>; break;
+    case 16: pk = conv_proj_kernel<16>; sk = conv_proj_slice_kernel<16>; break;
+    case 20: pk = conv_proj_kernel<20>; sk = conv_proj_slice_kernel<20>; break;
+    case 24: pk = conv_proj_kernel<24>; sk = conv_proj_slice_kernel<24>; break;
+    case 28: pk = conv_proj_kernel<28>; sk = conv_proj_slice_kernel<28>; break;
+    default: pk = conv_proj_kernel<32>; sk = conv_proj_slice_kernel<32>; break;
   }
   {
     const pxr_status os = kernel_occupancy((const void *)pk, kProjEnvs * 32, psmem, &per_sm);
@@ -413,6 +468,21 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   }
   cap = (int64_t)sms * per_sm;
   const int64_t groups = (batch + kProjEnvs - 1) / kProjEnvs;
+  const int n_slices = (K + kProjSlice - 1) / kProjSlice;
+  // small batches: one CTA per (env group, slice), then the slice sums are
+  // added (the same arithmetic as the one-CTA path); J <= kProjSlice keeps
+  // the parked sums inside the slice
+  if (n_slices > 1 && groups * n_slices <= cap && n_joints <= kProjSlice &&
+      debug_knob(kDbgNoSplit) == nullptr) {
+    sk<<<dim3((unsigned)groups, (unsigned)n_slices), kProjEnvs * 32, psmem, st>>>(
+        workspace, batch, K, proj, n_joints);
+    s = check_launch("conv_proj_slice_kernel");
+    if (s != PXR_OK) return s;
+    const int64_t n_out = batch * n_joints;
+    conv_proj_combine_kernel<<<(unsigned)((n_out + 127) / 128), 128, 0, st>>>(
+        workspace, batch, K, n_joints, out);
+    return check_launch("conv_proj_combine_kernel");
+  }
   grid = (int)(groups < cap ? groups : cap);
   pk<<<grid, kProjEnvs * 32, psmem, st>>>(workspace, batch, K, proj, n_joints, out);
   return check_launch("conv_proj_kernel");

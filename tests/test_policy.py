@@ -104,6 +104,22 @@ class TestConvStubGPU:
         assert torch.equal(B.conv_stub_forward(stub, obs[10:30]), full[10:30])
         assert bool((full.abs() <= 1.0).all())
 
+    def test_split_projection_rows_equal_one_cta_path(self, B, torch, knobs):
+        """Small batches split each env's projection over CTAs (one per
+        feature slice, the slice sums added in slice order by a second
+        kernel); large batches walk the slices in one CTA. The arithmetic is
+        the same, so a row is identical whichever path its batch takes."""
+        stub = B.ConvStub.create(84, 84, 3, 17, seed=5)
+        gen = torch.Generator(device="cuda").manual_seed(5)
+        obs = torch.randint(0, 256, (3000, 84, 84, 3), dtype=torch.uint8, device="cuda",
+                            generator=gen)
+        full = B.conv_stub_forward(stub, obs)  # (one CTA per 16 envs: too many for the split)
+        for i in (0, 7, 2999):
+            assert torch.equal(B.conv_stub_forward(stub, obs[i:i + 1])[0], full[i])
+        assert torch.equal(B.conv_stub_forward(stub, obs[100:164]), full[100:164])
+        knobs.set("PXR_DEBUG_NO_SPLIT", 1)
+        assert torch.equal(B.conv_stub_forward(stub, obs[:20]), full[:20])
+
     def test_matches_torch_conv2d_formulation(self, B, torch):
         """Weight-layout parity with the PyTorch formulation of the stub
         (SURVEY 8(f) row 3): conv weight (ky, kx, c, f) -> torch (f, c, ky,
