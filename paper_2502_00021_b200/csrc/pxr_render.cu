@@ -1333,6 +1333,10 @@ render_step_kernel(const RenderParams p) {
             const int excl = incl - len;
             const int NE = __shfl_sync(kFull, incl, 31);
             if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[3], NE);
+            // the chunk's pool slots, reserved at once (one atomic per chunk)
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&es.n_pool, NE);
+            base = __shfl_sync(kFull, base, 0);
 #pragma unroll 1
             for (int c0 = 0; c0 < NE; c0 += 32) {
               // span lane of candidate c = c0 + lane: the number of lanes whose
@@ -1348,15 +1352,12 @@ render_step_kernel(const RenderParams p) {
               const int o_x0 = __shfl_sync(kFull, x0, owner & 31);
               const int o_row = __shfl_sync(kFull, row, owner & 31);
               const int o_tri = __shfl_sync(kFull, j, owner & 31);
-              int base = 0;
-              if (lane == 0) base = atomicAdd(&es.n_pool, min(32, NE - c0));
-              base = __shfl_sync(kFull, base, 0);
               if (c < NE) {
                 const int px = o_x0 + (c - o_ex);
                 const uint32_t pix = (uint32_t)((o_row - y0) * p.W + px);
                 PXR_DCHECK(pix < (uint32_t)npx && o_tri < n_round && owner < 32);
-                if (base + lane < kPoolCap) {
-                  s_pool[base + lane] = pix | ((uint32_t)o_tri << 20);
+                if (base + c < kPoolCap) {
+                  s_pool[base + c] = pix | ((uint32_t)o_tri << 20);
                 } else {  // pool full: evaluated here
                   double z;
                   if (eval_exact(s_rec[o_tri], px, o_row, s_vxy64, s_viz, z))
