@@ -88,8 +88,9 @@ constexpr uint32_t kDecBit = 0x80000000u;
 // debug workload counters per env: live triangles, bbox-row units, non-empty
 // spans, candidate pixels, covered fragments, raster rounds, overflow rounds,
 // live triangles that cover no pixel centre, their bbox-row units, those of
-// them with a single bbox row
-constexpr int kStats = 10;
+// them with a single bbox row, bbox rows between each triangle's first and
+// last non-empty conservative span
+constexpr int kStats = 11;
 // debug phase timer slots (p.prof, tools/phase_prof.py): thread 0's clock at
 // each phase-ending barrier, accumulated per CTA
 constexpr int kProfSlots = 12;
@@ -1217,6 +1218,17 @@ render_step_kernel(const RenderParams p) {
           if (culled) S.ylo = __int_as_float(0x7f800000);  // every row span is empty
           S.py0 = (uint16_t)by0;
           S.pad = 0;
+          if (kWithStats && p.stats != nullptr) {
+            int f = -1, l = -1;
+            for (int row = by0; row <= by1; row++) {
+              int x0s;
+              if (row_span(S, row, wlim, x0s) > 0) {
+                if (f < 0) f = row;
+                l = row;
+              }
+            }
+            atomicAdd(&es.st[10], f < 0 ? 0 : l - f + 1);
+          }
           const uint32_t u0 = s_lrp[li] - rbase;
           S.row0 = u0;
           s_span[li - r0] = S;
@@ -1306,8 +1318,10 @@ render_step_kernel(const RenderParams p) {
               PXR_DCHECK(row >= y0 && row < y1);
               PXR_DCHECK(len == 0 || (x0 >= 0 && x0 + len <= p.W && len < 0x10000));
             }
-            if (kWithStats && p.stats != nullptr && lane == 0)
-              atomicAdd(&es.st[2], __popc(__ballot_sync(kFull, len > 0)));
+            if (kWithStats && p.stats != nullptr) {  // (every lane takes part in the ballot)
+              const int n_spans = __popc(__ballot_sync(kFull, len > 0));
+              if (lane == 0) atomicAdd(&es.st[2], n_spans);
+            }
             if (__all_sync(kFull, len <= 1)) {
               // every span is one pixel or empty (the common case): the
               // spans are the candidates, no expansion

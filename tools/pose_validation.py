@@ -34,7 +34,7 @@ STEPS = (0, 25, 50, 100, 200, 400)
 
 def measure(renderer, poses):
     B = poses.shape[0]
-    stats = torch.full((B, 10), -1, dtype=torch.int32, device="cuda")
+    stats = torch.full((B, 11), -1, dtype=torch.int32, device="cuda")  # kStats
     _native.set_debug("PXR_DEBUG_STATS_PTR", stats.data_ptr())
     _, depth = renderer.render(poses, floor_in_background=True, want_depth=True)
     torch.cuda.synchronize()

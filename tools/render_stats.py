@@ -20,7 +20,7 @@ import torch  # noqa: E402
 from paper_2502_00021_b200.bench_support import Workload  # noqa: E402
 
 NAMES = ("live_tris", "row_units", "spans", "candidates", "fragments", "rounds", "overflows",
-         "live_uncovering", "their_units", "their_1row")
+         "live_uncovering", "their_units", "their_1row", "trimmed_rows")
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--model", default="Humanoid")
