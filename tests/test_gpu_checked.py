@@ -75,3 +75,51 @@ def test_a_failed_check_traps_the_launch():
     out = r.stdout + r.stderr
     assert r.returncode == 3 and "launch failed" in out, out[-3000:]
     assert "PXR_DCHECK failed" in out and "p.nl" in out, out[-3000:]
+
+
+_STATS = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2502_00021_b200 import _native
+from paper_2502_00021_b200.bench_support import Workload
+assert _native.lib().pxr_build_checked() == 1
+K = 11  # csrc/pxr_render.cu kStats
+for model, mode, B, knob in (("Humanoid", "video", 300, None), ("Ant", "color", 300, None),
+                             ("HalfCheetah", "none", 40, "PXR_DEBUG_GRID"), ("Walker2d", "color", 5, None)):
+    if knob:
+        _native.set_debug(knob, 3)
+    w = Workload(model, B, mode)
+    st = torch.full((B, K), -1, dtype=torch.int32, device="cuda")
+    _native.set_debug("PXR_DEBUG_STATS_PTR", st.data_ptr())
+    w.render(w.poses(3), 3)
+    torch.cuda.synchronize()
+    _native.set_debug("PXR_DEBUG_STATS_PTR", None)
+    if knob:
+        _native.set_debug(knob, None)
+    s = st.cpu().numpy().astype(np.int64)
+    assert (s >= 0).all(), (model, "counters not written for every env")
+    live, units, spans, cand, frags, rounds, over, unc, unc_units, unc_1, trim = s.T
+    assert (over == 0).all(), model
+    if B * 2 > 148:  # one band per env (the split launch counts its last band only)
+        assert (live > 0).all() and (rounds >= 1).all(), model
+    assert (units >= live).all() and (spans <= units).all() and (trim <= units).all(), model
+    assert (cand >= spans).all() and (frags <= cand).all() and (unc <= live).all(), model
+    assert (unc_1 <= unc).all() and (unc_units >= unc).all(), model
+    print(model, mode, B, "live", live.mean(), "units", units.mean(), "cand", cand.mean())
+print("stats ok")
+"""
+
+
+def test_workload_counters_consistent():
+    """The checked build's per-env workload counters (tools/render_stats.py)
+    on the one-CTA-per-env, several-envs-per-CTA and split launches: written
+    for every env (a split env: its last band's counters) and mutually
+    consistent (live triangles <= bbox-row units,
+    spans <= units, candidates >= spans, fragments <= candidates, no
+    fragment-list overflow at the default budgets)."""
+    env = dict(os.environ, PXR_LIB_PATH=CHECKED)
+    r = subprocess.run([sys.executable, "-c", _STATS, REPO], cwd=REPO, env=env,
+                       capture_output=True, text=True, timeout=300)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "stats ok" in out, out[-3000:]
+    assert "PXR_DCHECK failed" not in out, out[-3000:]
