@@ -1,6 +1,6 @@
 """The parity suites again, through the checked build (libpxr_checked.so,
 -DPXR_CHECKED): every shared-memory index of the fused render kernel (record,
-span, row-owner, queue, fragment and pixel slots, the video texel and
+span, row-owner, candidate-pool, fragment and pixel slots, the video texel and
 byte-permute reads), the distractor / frame indices, the policy kernel's
 im2col and operand writes and the physics kernel's tree invariants are
 checked on the device, and a failed check traps the launch. Run in a child
