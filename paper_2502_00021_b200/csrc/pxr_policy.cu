@@ -408,15 +408,25 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   const int n_pos = ((height - kK) / kS + 1) * ((width - kK) / kS + 1);
   const int base = (Kc / 16) * ((kTcM / 8) * 256) + (Kc / 16) * ((kTcN / 8) * 256) +
                    2 * ((frame + 15) & ~15);
-  // the bf16 frame copy when it fits, else the per-chunk conversion
+  // the bf16 frame copy when it fits -- unless leaving it out lets more
+  // CTAs share an SM (84x84: 2 instead of 1, one CTA's operand build then
+  // overlaps the other's MMA wait: -8 % at 4096-16384 envs); else the
+  // per-chunk conversion (the same bf16 operands either way)
+  const DeviceFacts &df = device_facts();
+  static int smem_sm_dev[64] = {};
+  if (smem_sm_dev[df.device & 63] == 0)
+    cudaDeviceGetAttribute(&smem_sm_dev[df.device & 63], cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                           df.device);
+  const int smem_sm = smem_sm_dev[df.device & 63];
   const int with_table = base + ((4 * n_pos + 15) & ~15);
-  const int use_fb = with_table + ((2 * frame + 15) & ~15) <= 220 * 1024;
-  const int smem = use_fb ? with_table + ((2 * frame + 15) & ~15) : with_table;
+  const int with_fb = with_table + ((2 * frame + 15) & ~15);
+  int use_fb = with_fb <= 220 * 1024;
+  if (use_fb && smem_sm / (with_table + 2048) > smem_sm / (with_fb + 2048)) use_fb = 0;
+  const int smem = use_fb ? with_fb : with_table;
   if (smem > 220 * 1024) return set_unsupported("observation too large for the policy kernel");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // the full shared-memory carveout (frames + bf16 frame + operands), set
   // once per device; the dynamic-smem attribute through the launch cache
-  const DeviceFacts &df = device_facts();
   static bool carveout_set[64] = {};
   if (!carveout_set[df.device & 63]) {
     cudaError_t e = cudaFuncSetAttribute(conv_feat_tc_kernel,
@@ -433,11 +443,6 @@ extern "C" pxr_status pxr_conv_stub_forward(const uint8_t *obs, int64_t batch, i
   const int sms = df.num_sms;
   // CTAs per SM from the shared memory per SM (the occupancy query does not
   // see the carveout preference set above)
-  static int smem_sm_dev[64] = {};
-  if (smem_sm_dev[df.device & 63] == 0)
-    cudaDeviceGetAttribute(&smem_sm_dev[df.device & 63], cudaDevAttrMaxSharedMemoryPerMultiprocessor,
-                           df.device);
-  const int smem_sm = smem_sm_dev[df.device & 63];
   per_sm = smem_sm / (smem + 2048);
   if (per_sm > 2048 / kTcThreads) per_sm = 2048 / kTcThreads;
   if (per_sm < 1) per_sm = 1;
