@@ -99,6 +99,16 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// One thread's shared-memory atomic add, returning the old value. atomicAdd
+// would be wrapped in the compiler's warp aggregation (vote, leader, shuffle:
+// ~12 instructions and a lane-id read on the critical path) even where a
+// single lane issues it.
+__device__ __forceinline__ int smem_atomic_add(int *p, int v) {
+  int old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
+
 // Make generic-proxy smem writes visible to the async (TMA) proxy.
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -1329,7 +1329,7 @@ render_step_kernel(const RenderParams p) {
               const int n = __popc(sm);
               if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[3], n);
               int base = 0;
-              if (lane == 0 && n > 0) base = atomicAdd(&es.n_pool, n);
+              if (lane == 0 && n > 0) base = smem_atomic_add(&es.n_pool, n);
               base = __shfl_sync(kFull, base, 0) + __popc(sm & lanemask_lt);
               if (len > 0) {
                 const uint32_t pix = (uint32_t)((row - y0) * p.W + x0);
@@ -1349,7 +1349,7 @@ render_step_kernel(const RenderParams p) {
             if (kWithStats && p.stats != nullptr && lane == 0) atomicAdd(&es.st[3], NE);
             // the chunk's pool slots, reserved at once (one atomic per chunk)
             int base = 0;
-            if (lane == 0) base = atomicAdd(&es.n_pool, NE);
+            if (lane == 0) base = smem_atomic_add(&es.n_pool, NE);
             base = __shfl_sync(kFull, base, 0);
 #pragma unroll 1
             for (int c0 = 0; c0 < NE; c0 += 32) {
