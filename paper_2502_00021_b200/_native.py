@@ -8,6 +8,7 @@ requested, the call raises -- the hot path never silently runs on the CPU.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import subprocess
@@ -203,19 +204,33 @@ def require_cuda():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_NO_SCOPE = contextlib.nullcontext()
+
+
 def device_scope(device):
     """Make ``device`` current for the launches inside (kernels go to that
-    device's current stream; the library's per-device launch facts follow)."""
+    device's current stream; the library's per-device launch facts follow).
+    Already current (the common case): no context switch at all."""
     import torch
 
+    idx = device.index if isinstance(device, torch.device) else None
+    if idx is not None and idx == torch._C._cuda_getDevice():
+        return _NO_SCOPE
     return torch.cuda.device(device)
 
 
 def stream_ptr(stream=None) -> int:
+    """Raw cudaStream_t of ``stream``, or of the current device's current
+    stream (read straight from the CUDA state: the per-launch host cost of the
+    small-batch loop)."""
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    if stream is not None:
+        return int(stream.cuda_stream)
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return int(raw(torch._C._cuda_getDevice()))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 def ptr(t) -> int | None:

@@ -330,7 +330,7 @@ class RobotRenderer:
 
         if poses.dtype != torch.float64 or poses.device.type != "cuda":
             raise ValueError("poses must be a float64 CUDA tensor")
-        if torch.device(poses.device) != torch.device(self.device):
+        if poses.device != self.device:  # (both carry an index)
             raise ValueError(f"poses are on {poses.device}, the renderer on {self.device}")
         with _native.device_scope(self.device):
             return self._render(poses, floor_in_background, dist, pack, advance, keys, done,
